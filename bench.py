@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the AAR chain-prox hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl ours|reference]
+
+A *step* is one AAR iteration (every chain family's exact weighted 1D-TV prox
+plus the reflect/average/primal update and the step-norm monitor) over the
+whole grid of BASELINE.json's workload (default cfg4: 3D-6 256^3, fp32 state).
+``value`` = grid-node prox updates per second = r * n * K * N / t, with t the
+max over ranks of the CUDA-event time of K steps on data resident in HBM
+(working set > L2, so no flush is needed).  ``e2e`` runs the same K steps
+through the public API ``paracut_b200.solve`` from host numpy arrays
+(upload, cold start, shadow + certificate at k=0 and k=K, labels and primal
+read back), wall clock.  ``roofline`` covers the dominant kernel (the chain
+family prox kernel with the largest share of the step), timed live with CUDA
+events around each launch inside the timed region.  ``cpu_baseline`` is the
+oracle's C restatement of the reference loop (bitwise equal to it) on a slab
+sample of the same instance, all host threads.
+
+N > 1: every rank solves its own seeded instance (replicas, weak scaling; no
+data-path collective -- the slab-sharded single-instance path is SURVEY 8(e)
+and not in this round).  ``--impl reference`` times the CPU reference port on
+rank 0 only; other ranks exit 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-node TV-prox updates/sec per AAR iteration"
+CPU_SAMPLE_NODES = 1 << 22
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="cfg4")
+    ap.add_argument("--precision", default=None, choices=(None, "f32", "f64"))
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def crop_axis0(g, nodes_cap):
+    """Slab of the instance along the slowest axis with <= nodes_cap nodes."""
+    from paracut_b200.graph import GridEnergy, DIRECTIONS
+    dims = tuple(g.dims)
+    plane = int(np.prod(dims[1:]))
+    rows = max(2, min(dims[0], nodes_cap // plane))
+    if rows >= dims[0]:
+        return g
+    nd = (rows,) + dims[1:]
+    w = g.w.reshape(dims)[:rows].ravel()
+    dws = []
+    for d, a in zip(DIRECTIONS[g.connectivity], g.dir_weights):
+        dws.append(np.ascontiguousarray(a[:rows - abs(d[0])]))
+    return GridEnergy(nd, g.connectivity, np.ascontiguousarray(w), dws)
+
+
+def cpu_port_rate(g, iters, warm=1):
+    """(updates/s, threads, sample) for the oracle's C port of the reference loop."""
+    from oracle import oracle as orc
+    sample = crop_axis0(g, CPU_SAMPLE_NODES)
+    threads = orc.max_threads()
+    run = orc.AARRunner(sample, threads=threads)
+    run.run(warm, final_shadow=False)
+    t0 = time.perf_counter()
+    run.run(iters, final_shadow=False)
+    dt = time.perf_counter() - t0
+    rate = run.r * run.n * iters / dt
+    desc = ("%s slab %s of the workload instance, %d AAR iterations (fp64, bitwise the "
+            "reference's arithmetic), oracle/paracut_oracle.c OpenMP over chains"
+            % (g.connectivity, "x".join(map(str, sample.dims)), iters))
+    return rate, threads, desc, dt
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    from paracut_b200.instances import CONFIGS, make_instance
+    if rank != 0:
+        return
+    spec = CONFIGS[args.workload]
+    g = make_instance(spec, seed=args.seed)
+    from oracle import oracle as orc
+    sample = crop_axis0(g, CPU_SAMPLE_NODES)
+    threads = orc.max_threads()
+    run = orc.AARRunner(sample, threads=threads)
+    run.run(max(args.warmup, 1), final_shadow=False)
+    t0 = time.perf_counter()
+    run.run(args.steps, final_shadow=False)
+    dt = time.perf_counter() - t0
+    value = run.r * run.n * args.steps / dt
+    desc = ("%s slab %s of the %s instance (seed %d), fp64; each step one AAR iteration"
+            % (g.connectivity, "x".join(map(str, sample.dims)), args.workload, args.seed))
+    line = {
+        "metric": METRIC, "value": value, "unit": "updates/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json generator)",
+        "config": {"workload": args.workload, "dims": list(spec.dims),
+                   "connectivity": spec.connectivity, "sample_dims": list(sample.dims)},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paracut_b200 as pc
+    from paracut_b200 import _native
+    from paracut_b200.instances import CONFIGS, make_instance, algorithmic_bytes
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = CONFIGS[args.workload]
+    precision = args.precision or ("f64" if spec.dtype == "f64" else "f32")
+    b = 8 if precision == "f64" else 4
+    g = make_instance(spec, seed=args.seed + rank)
+    S = _native.GridSolver(g, precision=precision, device=local)
+    r, n = S.r, S.n
+    stream = torch.cuda.Stream(device=local)
+    S.set_stream(stream.cuda_stream)
+    S.init_cold()
+    S.run(args.warmup, norms=False)
+    S.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    S.reset_launch_count()
+    S.set_profiling(True)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    S.run(args.steps, norms=False)
+    ev1.record(stream)
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    fam_ms, fam_cnt = S.profile_read()
+    S.set_profiling(False)
+    launches = S.launch_count()
+    clk = clocks.stop()
+    torch.cuda.synchronize()
+
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * r * n * args.steps / (ms_max / 1e3)
+
+    # roofline of the dominant kernel: per-launch algorithmic bytes / mean duration
+    pk, pk_kind = peaks()
+    fam = int(np.argmax(fam_ms))
+    nedge = [int(np.count_nonzero(a)) for a in g.dir_weights]
+    fam_edges = _family_edges(g)
+    per_launch = b * (2 * n + fam_edges[fam])
+    mean_ms = fam_ms[fam] / max(int(fam_cnt[fam]), 1)
+    achieved = per_launch / (mean_ms / 1e3) / 1e9
+    traffic = _ncu_traffic(args.workload, fam)
+    B_iter = algorithmic_bytes(g, r, b)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
+            "frac": achieved / pk, "traffic": traffic,
+            "kernel": "family %d (%s) prox sweep" % (fam, pc.decompose_grid(g).families[fam]),
+            "bytes_per_launch": per_launch, "mean_launch_ms": mean_ms,
+            "share_of_step": float(fam_ms[fam] / ms) if ms > 0 else None,
+            "peak_kind": pk_kind,
+            "per_family_ms": [float(v / max(int(c), 1)) for v, c in zip(fam_ms, fam_cnt)],
+            "iteration_achieved_gbs": B_iter * args.steps / (ms / 1e3) / 1e9,
+            "iteration_bytes": B_iter}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, threads, desc, _ = cpu_port_rate(g, args.cpu_iters)
+        cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
+               "sample": desc}
+
+    e2e = None
+    if not args.no_e2e:
+        S.close()
+        del S
+        torch.cuda.synchronize()
+        dims, wbytes = g.dims, g.w.nbytes + sum(a.nbytes for a in g.dir_weights)
+        cfg = pc.SolverConfig(algorithm="aar", max_iters=args.steps,
+                              check_every=args.steps + 1, precision=precision,
+                              device=local)
+        t0 = time.perf_counter()
+        res = pc.solve(g, pc.decompose_grid(g), cfg)
+        _ = res.labeling.sum()
+        wall = time.perf_counter() - t0
+        wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+        wall = float(wt.item())
+        nb = (n + 7) // 8
+        d2h = n + 8 * n + 2 * nb + 2 * 8 * 4
+        e2e = {"value": world * r * n * args.steps / wall, "unit": "updates/s",
+               "h2d_bytes_per_step": wbytes / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+               "wall_s": wall, "certified": bool(res.certified), "gap": float(res.gap)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "storage_dtype": "f32" if precision == "f32" else "f64",
+            "data": "synthetic (BASELINE.json generator, seed %d+rank)" % args.seed,
+            "config": {"workload": args.workload, "dims": list(spec.dims),
+                       "connectivity": spec.connectivity, "r": r, "n": n,
+                       "precision": precision, "step": "1 AAR iteration",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "working set %.0f MB > 126 MB L2, no flush needed"
+                             % (B_iter / 1e6)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _family_edges(g):
+    """|E_j| per family (nonzero edges each chain family owns), decompose_grid order."""
+    dw = g.dir_weights
+    nz = [int(np.count_nonzero(a)) for a in dw]
+    if g.connectivity == "2D-4" or g.connectivity == "3D-6":
+        return nz
+    # 2D-8: zig-zag phase 0 takes d1 on even columns, d2 on odd; phase 1 the rest
+    d1, d2 = dw[2], dw[3]
+    even = (np.arange(d1.shape[1]) % 2) == 0
+    z0 = int(np.count_nonzero(d1[:, even])) + int(np.count_nonzero(d2[:, ~even]))
+    z1 = int(np.count_nonzero(d2[:, even])) + int(np.count_nonzero(d1[:, ~even]))
+    return [nz[0], nz[1], z0, z1]
+
+
+def _ncu_traffic(workload, fam):
+    """dram bytes per launch of that kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(workload, {}).get(str(fam))
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/*
+ * paracut_b200.h -- C ABI of the B200 AAR chain-prox path.
+ *
+ * Plain pointers and sizes only (no torch types); every function returns 0 on
+ * success or a negative PCB_E* code, with a message in pcb_last_error()
+ * (thread-local).  Host arrays are caller-owned and copied; device buffers
+ * are owned by the opaque solver handle.  One handle = one CUDA stream; a
+ * handle is not re-entrant, distinct handles may be used from distinct
+ * threads.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/paracut/<file>:<line>); INTEGRATION.md shows the
+ * ctypes binding a maintainer would add to the reference.
+ */
+#ifndef PARACUT_B200_H
+#define PARACUT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCB_OK 0
+#define PCB_E_ARG -1      /* invalid argument  -> ValueError in Python   */
+#define PCB_E_CUDA -2     /* CUDA runtime error -> RuntimeError           */
+#define PCB_E_STATE -3    /* call out of order  -> RuntimeError           */
+#define PCB_E_NOMEM -4    /* device allocation failed -> MemoryError      */
+
+/* connectivity codes, graph.py:18 CONNECTIVITIES order */
+#define PCB_CONN_2D4 0
+#define PCB_CONN_2D8 1
+#define PCB_CONN_3D6 2
+
+/* state precision
+ * PCB_F64: AAR point z kept in fp64 and updated with the reference's exact
+ *          operation order -> iterates bitwise equal to solvers.py:289-298.
+ * PCB_F32: shadow p_j stored fp32, shared drift c fp64, primal x fp32;
+ *          z_j = p_j + c; all prox arithmetic in fp64 (SURVEY 8(a) a6 form). */
+#define PCB_F64 0
+#define PCB_F32 1
+
+typedef struct pcb_solver pcb_solver;
+
+const char *pcb_last_error(void);
+int pcb_version(void);
+int pcb_device_count(int *count);
+
+/* ---- operator level ------------------------------------------------------
+ * Replaces _kernels.prox_chains(node_idx, chain_ptr, edge_w, c_lo, c_hi, v,
+ * out, as_projection) (_kernels.py:145-180).  Host buffers; chains
+ * [c_lo, c_hi) of one CSR class; out[node_idx[..]] <- v - prox (projection)
+ * or prox.  n = len(v) = len(out); edges of chain c start at
+ * chain_ptr[c] - c (_kernels.py:171). */
+int pcb_prox_chains(const int64_t *node_idx, const int64_t *chain_ptr, const double *edge_w,
+                    int64_t c_lo, int64_t c_hi, int64_t n_nodes, int64_t n_idx,
+                    int64_t n_edges, const double *v, double *out, int as_projection,
+                    int device);
+
+/* Replaces tv1d.tv1d_prox (tv1d.py:42-69) batched over a CSR of signals:
+ * signal c is s[ptr[c]:ptr[c+1]], its weights a[ptr[c]-c : ptr[c+1]-c-1]. */
+int pcb_tv1d_prox_batch(const double *s, const double *a, const int64_t *ptr, int64_t nchains,
+                        double *x, int device);
+
+/* Replaces projections.project_L (projections.py:107-122) for an arbitrary
+ * decomposition: w[n], degree[n], support[r*n] (0/1), v[r*n] -> out[r*n],
+ * lam_j = (v_j + (w - sum_k v_k) / d) * support_j.  PCB_E_ARG when w has
+ * mass on a node of degree 0 (projections.py:115-117). */
+int pcb_project_L(const double *w, const int64_t *degree, const uint8_t *support, int r,
+                  int64_t n, const double *v, double *out, int device);
+
+/* ---- grid solver ---------------------------------------------------------
+ * Replaces GridEnergy + decompose_grid + the solve_aar loop
+ * (graph.py:125-161, decompose.py:186-200, solvers.py:272-307).
+ * dims: ndim = 2 or 3 sizes (C order); w: n unaries; dir_weights[k]: dense
+ * per-direction arrays in graph.DIRECTIONS order with the shapes of
+ * graph.direction_shape. */
+int pcb_create(const int64_t *dims, int ndim, int conn, int precision, const double *w,
+               const double *const *dir_weights, int device, pcb_solver **out);
+int pcb_destroy(pcb_solver *h);
+/* r (number of chain families) and n */
+int pcb_shape(const pcb_solver *h, int *r, int64_t *n);
+/* Use this CUDA stream (cudaStream_t as uintptr) for all later launches. */
+int pcb_set_stream(pcb_solver *h, uintptr_t stream);
+int pcb_synchronize(pcb_solver *h);
+
+/* z0 = Pi_L(0) = w/r per class (solvers.py:284-285). */
+int pcb_init_cold(pcb_solver *h);
+/* Warm start / readback of the AAR point z, r*n fp64 class-major
+ * (DualState.z, projections.py:28-44; solvers.py:150-165). */
+int pcb_set_z(pcb_solver *h, const double *z);
+int pcb_get_z(pcb_solver *h, double *z);
+
+/* iters plain AAR iterations z <- z + Pi_L(2 Pi_K z - z) - Pi_K z
+ * (solvers.py:295-298); step_norms (nullable, device-accumulated, copied
+ * out at the end) receives ||z_{k+1} - z_k|| per iteration. */
+int pcb_aar_run(pcb_solver *h, int64_t iters, double *step_norms);
+
+/* Shadow y = Pi_K(z) into the handle's shadow buffer (projections.py:89-104);
+ * does not change z.  y_out (nullable, r*n) and s_out (nullable, n,
+ * aggregate in class order, projections.py:133-137) are copied to host. */
+int pcb_shadow(pcb_solver *h, double *y_out, double *s_out);
+/* Copy the current shadow (from the last pcb_shadow*) to host without
+ * recomputing it (final DualState.y, solvers.py:307). */
+int pcb_shadow_get(pcb_solver *h, double *y_out);
+/* pcb_shadow plus *delta = ||y_new - y_prev|| against the shadow that was
+ * current before the call (-1 if there was none): the dual_tol test of
+ * solvers.py:300-306. */
+int pcb_shadow_delta(pcb_solver *h, double *delta);
+/* Apply one AAR update using the current shadow (after pcb_shadow):
+ * z <- z + Pi_L(2y - z) - y; writes ||dz|| to *step_norm (nullable). */
+int pcb_apply(pcb_solver *h, double *step_norm);
+
+/* Certificates on the current shadow (solvers.py:170-182, certify.py:31-47):
+ * x = w - s, labels_t = (x > thr[t]) for nthr <= 8 thresholds; per threshold
+ * energy f(lab) - w.lab, gap = energy - sum min(s - w, 0); *dual_obj =
+ * 0.5||w||^2 - 0.5||s - w||^2.  Labels and x stay on device ("current"). */
+int pcb_check(pcb_solver *h, int nthr, const double *thr, double *energy, double *gap,
+              double *dual_obj);
+/* Copy the current check's labels for threshold t (uint8[n], or packed bits
+ * MSB-first like np.packbits when packed=1) and x (fp64[n]) to host (each nullable). */
+int pcb_get_check(pcb_solver *h, int t, uint8_t *labels, int packed, double *x);
+/* Keep the current check as the best iterate / fetch the kept one. */
+int pcb_keep_best(pcb_solver *h, int t);
+int pcb_get_best(pcb_solver *h, uint8_t *labels, double *x);
+
+/* Pi_K of an arbitrary r*n host vector with this grid's decomposition
+ * (project_K, projections.py:89-104); fp64 exact kernels regardless of the
+ * handle precision. */
+int pcb_project_K(pcb_solver *h, const double *v, double *out);
+
+/* Kernel timing for the roofline: while enabled, every chain-family prox
+ * launch is bracketed by CUDA events on the handle stream; pcb_profile_read
+ * synchronises, returns summed milliseconds and launch counts per family
+ * (r entries each, family order of decompose_grid) and clears the record. */
+int pcb_set_profiling(pcb_solver *h, int on);
+int pcb_profile_read(pcb_solver *h, double *ms, int64_t *launches);
+
+/* Launch counting for the bench contract: kernels launched since the last
+ * reset (our kernels only). */
+int64_t pcb_launch_count(const pcb_solver *h);
+void pcb_reset_launch_count(pcb_solver *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

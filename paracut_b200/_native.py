@@ -1,0 +1,292 @@
+"""ctypes binding of ``libparacut_b200.so`` (the C ABI in include/paracut_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA
+device is visible, every entry point raises.  Build the library with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``python -m
+paracut_b200.build``); the .so is written in-tree under ``paracut_b200/_lib``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
+
+PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
+CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
+PRECISIONS = {"f64": 0, "f32": 1}
+
+_lib = None
+_lock = threading.Lock()
+
+P = ctypes.c_void_p
+I64 = ctypes.c_int64
+INT = ctypes.c_int
+DBL_P = ctypes.POINTER(ctypes.c_double)
+
+
+class NativeLibraryMissing(ImportError):
+    pass
+
+
+def _declare(L):
+    L.pcb_last_error.restype = ctypes.c_char_p
+    L.pcb_version.restype = INT
+    L.pcb_device_count.argtypes = [ctypes.POINTER(INT)]
+    L.pcb_prox_chains.argtypes = [P, P, P, I64, I64, I64, I64, I64, P, P, INT, INT]
+    L.pcb_tv1d_prox_batch.argtypes = [P, P, P, I64, P, INT]
+    L.pcb_create.argtypes = [P, INT, INT, INT, P, P, INT, ctypes.POINTER(P)]
+    L.pcb_destroy.argtypes = [P]
+    L.pcb_shape.argtypes = [P, ctypes.POINTER(INT), ctypes.POINTER(I64)]
+    L.pcb_set_stream.argtypes = [P, ctypes.c_size_t]
+    L.pcb_synchronize.argtypes = [P]
+    L.pcb_init_cold.argtypes = [P]
+    L.pcb_set_z.argtypes = [P, P]
+    L.pcb_get_z.argtypes = [P, P]
+    L.pcb_aar_run.argtypes = [P, I64, P]
+    L.pcb_shadow.argtypes = [P, P, P]
+    L.pcb_apply.argtypes = [P, P]
+    L.pcb_shadow_get.argtypes = [P, P]
+    L.pcb_shadow_delta.argtypes = [P, P]
+    L.pcb_check.argtypes = [P, INT, P, P, P, P]
+    L.pcb_get_check.argtypes = [P, INT, P, INT, P]
+    L.pcb_keep_best.argtypes = [P, INT]
+    L.pcb_get_best.argtypes = [P, P, P]
+    L.pcb_project_K.argtypes = [P, P, P]
+    L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
+    L.pcb_set_profiling.argtypes = [P, INT]
+    L.pcb_profile_read.argtypes = [P, P, P]
+    L.pcb_launch_count.argtypes = [P]
+    L.pcb_launch_count.restype = I64
+    L.pcb_reset_launch_count.argtypes = [P]
+    L.pcb_reset_launch_count.restype = None
+
+
+EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains",
+           "pcb_tv1d_prox_batch", "pcb_create", "pcb_destroy", "pcb_shape", "pcb_set_stream",
+           "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
+           "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
+           "pcb_get_best", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_reset_launch_count")
+
+
+def lib():
+    """Load the native library (raises NativeLibraryMissing if it is not built)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise NativeLibraryMissing(
+                        "paracut_b200 native library not built (%s); run "
+                        "`python -m paracut_b200.build`" % LIB_PATH)
+                L = ctypes.CDLL(LIB_PATH)
+                _declare(L)
+                _lib = L
+    return _lib
+
+
+def check(rc):
+    if rc == 0:
+        return
+    msg = lib().pcb_last_error().decode(errors="replace")
+    if rc == PCB_E_ARG:
+        raise ValueError(msg)
+    if rc == PCB_E_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError("paracut_b200: %s (code %d)" % (msg, rc))
+
+
+def ptr(a):
+    return None if a is None else a.ctypes.data_as(P)
+
+
+def device_count():
+    c = INT(0)
+    check(lib().pcb_device_count(ctypes.byref(c)))
+    return int(c.value)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class GridSolver:
+    """Owns one device-resident grid instance + AAR state (pcb_solver*)."""
+
+    def __init__(self, g, precision="f64", device=0):
+        if precision not in PRECISIONS:
+            raise ValueError("precision must be one of %r" % (tuple(PRECISIONS),))
+        L = lib()
+        self.precision = precision
+        self.device = int(device)
+        self.dims = tuple(int(d) for d in g.dims)
+        dims = np.asarray(self.dims, dtype=np.int64)
+        w = _f64(g.w)
+        dws = [_f64(a) for a in g.dir_weights]
+        arr = (P * 4)(*([ptr(a) for a in dws] + [None] * (4 - len(dws))))
+        self._keep = (dims, w, dws)
+        h = P()
+        check(L.pcb_create(ptr(dims), len(self.dims), CONN_CODES[g.connectivity],
+                           PRECISIONS[precision], ptr(w), arr, self.device, ctypes.byref(h)))
+        self._keep = None
+        self._h = h
+        r, n = INT(0), I64(0)
+        check(L.pcb_shape(h, ctypes.byref(r), ctypes.byref(n)))
+        self.r, self.n = int(r.value), int(n.value)
+
+    # -- lifecycle
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            lib().pcb_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        if not self._h:
+            raise RuntimeError("solver handle is closed")
+        return self._h
+
+    # -- state
+    def set_stream(self, stream_ptr):
+        check(lib().pcb_set_stream(self.handle, int(stream_ptr)))
+
+    def synchronize(self):
+        check(lib().pcb_synchronize(self.handle))
+
+    def init_cold(self):
+        check(lib().pcb_init_cold(self.handle))
+
+    def set_z(self, z):
+        z = _f64(z)
+        if z.shape != (self.r, self.n):
+            raise ValueError("warm start shape %r, expected %r" % (z.shape, (self.r, self.n)))
+        check(lib().pcb_set_z(self.handle, ptr(z)))
+
+    def get_z(self):
+        z = np.empty((self.r, self.n))
+        check(lib().pcb_get_z(self.handle, ptr(z)))
+        return z
+
+    def run(self, iters, norms=True):
+        out = np.empty(max(int(iters), 1)) if norms else None
+        check(lib().pcb_aar_run(self.handle, int(iters), ptr(out)))
+        return out[:int(iters)] if norms else None
+
+    def shadow(self, want_y=False, want_s=False):
+        y = np.empty((self.r, self.n)) if want_y else None
+        s = np.empty(self.n) if want_s else None
+        check(lib().pcb_shadow(self.handle, ptr(y), ptr(s)))
+        return y, s
+
+    def shadow_get(self):
+        y = np.empty((self.r, self.n))
+        check(lib().pcb_shadow_get(self.handle, ptr(y)))
+        return y
+
+    def shadow_delta(self):
+        d = np.empty(1)
+        check(lib().pcb_shadow_delta(self.handle, ptr(d)))
+        return float(d[0])
+
+    def apply(self):
+        out = np.empty(1)
+        check(lib().pcb_apply(self.handle, ptr(out)))
+        return float(out[0])
+
+    def check(self, thresholds):
+        thr = _f64(thresholds)
+        T = thr.size
+        e, gp, d = np.empty(T), np.empty(T), np.empty(1)
+        check(lib().pcb_check(self.handle, T, ptr(thr), ptr(e), ptr(gp), ptr(d)))
+        return e, gp, float(d[0])
+
+    def check_labels(self, t, packed=False):
+        nb = (self.n + 7) // 8 if packed else self.n
+        lab = np.empty(nb, dtype=np.uint8)
+        check(lib().pcb_get_check(self.handle, int(t), ptr(lab), int(bool(packed)), None))
+        return lab
+
+    def check_x(self, t=0):
+        x = np.empty(self.n)
+        check(lib().pcb_get_check(self.handle, int(t), None, 0, ptr(x)))
+        return x
+
+    def keep_best(self, t):
+        check(lib().pcb_keep_best(self.handle, int(t)))
+
+    def get_best(self):
+        lab = np.empty(self.n, dtype=np.uint8)
+        x = np.empty(self.n)
+        check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
+        return lab, x
+
+    def project_K(self, v):
+        v = _f64(v)
+        if v.shape != (self.r, self.n):
+            raise ValueError("expected shape %r" % ((self.r, self.n),))
+        out = np.empty_like(v)
+        check(lib().pcb_project_K(self.handle, ptr(v), ptr(out)))
+        return out
+
+    def set_profiling(self, on):
+        check(lib().pcb_set_profiling(self.handle, int(bool(on))))
+
+    def profile_read(self):
+        ms = np.zeros(self.r)
+        cnt = np.zeros(self.r, dtype=np.int64)
+        check(lib().pcb_profile_read(self.handle, ptr(ms), ptr(cnt)))
+        return ms, cnt
+
+    def launch_count(self):
+        return int(lib().pcb_launch_count(self.handle))
+
+    def reset_launch_count(self):
+        lib().pcb_reset_launch_count(self.handle)
+
+
+def prox_chains(node_idx, chain_ptr, edge_w, c_lo, c_hi, v, out, as_projection, device=0):
+    """GPU replacement of _kernels.prox_chains (in-place on ``out``)."""
+    node_idx = np.ascontiguousarray(node_idx, dtype=np.int64)
+    chain_ptr = np.ascontiguousarray(chain_ptr, dtype=np.int64)
+    edge_w = _f64(edge_w)
+    v = _f64(v)
+    if out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a contiguous float64 array")
+    check(lib().pcb_prox_chains(ptr(node_idx), ptr(chain_ptr),
+                                ptr(edge_w) if edge_w.size else None, int(c_lo), int(c_hi),
+                                v.size, node_idx.size, edge_w.size, ptr(v), ptr(out),
+                                int(bool(as_projection)), int(device)))
+
+
+def tv1d_batch(s, a, ptr_, device=0):
+    s = _f64(s)
+    a = _f64(a)
+    ptr_ = np.ascontiguousarray(ptr_, dtype=np.int64)
+    x = np.empty_like(s)
+    check(lib().pcb_tv1d_prox_batch(ptr(s), ptr(a) if a.size else None, ptr(ptr_),
+                                    ptr_.size - 1, ptr(x), int(device)))
+    return x
+
+
+def project_L_general(w, degree, support, v, device=0):
+    """Pi_L for an arbitrary (hand-built) decomposition (projections.py:107-122)."""
+    w = _f64(w)
+    v = _f64(v)
+    degree = np.ascontiguousarray(degree, dtype=np.int64)
+    support = np.ascontiguousarray(support, dtype=np.uint8)
+    r, n = v.shape
+    out = np.empty_like(v)
+    check(lib().pcb_project_L(ptr(w), ptr(degree), ptr(support), int(r), int(n), ptr(v),
+                              ptr(out), int(device)))
+    return out

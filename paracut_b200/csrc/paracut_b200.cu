@@ -1,0 +1,1544 @@
+// paracut_b200.cu -- sm_100a kernels and the C ABI (include/paracut_b200.h)
+// for the AAR chain-prox hot path of arXiv 1503.01563 (reference: paracut).
+//
+// Layout in HBM:
+//   node arrays      n entries, C order of dims (w, c, x, G, labels, z_j, y_j)
+//   family weights   Wf_j[i * C_j + c]: edge i of chain c, chain-interleaved
+//                    so that threads owning adjacent chains read adjacent words
+//   direction weights natural graph.direction_shape arrays (certificates)
+//
+// Kernels:
+//   k_family_exact   fp64 prox of one chain family, z_j -> y_j = z_j - prox
+//                    (projections.py:89-104 / _kernels.py:145-180)
+//   k_update_exact   z += Pi_L(2y - z) - y in the reference's operation order
+//                    (solvers.py:295-298, projections.py:107-122)
+//   k_family_fast    fused fp32-state sweep: prox of z_j = p_j + c, p_j in
+//                    place, accumulator G, last family applies the drift update
+//   k_apply_fast     check-iteration update from an fp64 shadow
+//   k_check_nodes / k_check_edges   threshold, unary, dual, cut partials
+//   k_reduce_*       deterministic fixed-order final reductions
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/paracut_b200.h"
+#include "taut_string.cuh"
+
+#define PCB_VERSION 1
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      (void)cudaGetLastError();                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? PCB_E_NOMEM : PCB_E_CUDA, "%s: %s (%s:%d)", \
+                  #expr, cudaGetErrorString(e_), __FILE__, __LINE__);                      \
+    }                                                                                      \
+  } while (0)
+
+#define LAUNCH_CHECK(h)                                                                    \
+  do {                                                                                     \
+    cudaError_t e_ = cudaGetLastError();                                                   \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(PCB_E_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), __FILE__, \
+                  __LINE__);                                                               \
+    if (h) (h)->launches++;                                                                \
+  } while (0)
+
+constexpr int HC = 8;          // hull entries kept in shared memory per thread
+constexpr int FAM_BLOCK = 128;  // threads (chains) per block in family kernels
+constexpr int RED_BLOCK = 256;
+constexpr int MAXR = 4;
+constexpr int MAXT = 8;         // thresholds per check
+
+// ----------------------------------------------------------------- geometry
+
+enum FamKind { K_ROW2 = 0, K_COL2, K_ZZ0, K_ZZ1, K_X3, K_Y3, K_Z3 };
+
+// node(c, i) = (c / cdiv) * chi + (c % cdiv) * clo + i * ns + zz * ((i + phase) & 1)
+struct Fam {
+  int kind;
+  int m;          // nodes per chain
+  int64_t C;      // chains
+  int64_t cdiv, chi, clo, ns, zz;
+  int phase;
+};
+
+__device__ __forceinline__ int64_t fam_base(const Fam& F, int64_t c) {
+  return (c / F.cdiv) * F.chi + (c % F.cdiv) * F.clo;
+}
+__device__ __forceinline__ int64_t fam_node(const Fam& F, int64_t b, int i) {
+  return b + (int64_t)i * F.ns + F.zz * (int64_t)((i + F.phase) & 1);
+}
+
+struct Dims {
+  int nd;
+  int64_t d[3];
+  int conn;
+};
+
+// Which direction array and element hold edge i of chain c (decompose.py:142-183).
+__device__ __forceinline__ void fam_edge(const Fam& F, const Dims& D, int64_t c, int i, int* dir,
+                                         int64_t* idx) {
+  switch (F.kind) {
+    case K_ROW2:  // dir 0, shape (H, W-1)
+      *dir = 0;
+      *idx = c * (D.d[1] - 1) + i;
+      return;
+    case K_COL2:  // dir 1, shape (H-1, W)
+      *dir = 1;
+      *idx = (int64_t)i * D.d[1] + c;
+      return;
+    case K_ZZ0:  // even edge: d1 (dir 2), odd: d2 (dir 3); shape (H-1, W-1)
+      *dir = (i & 1) ? 3 : 2;
+      *idx = c * (D.d[1] - 1) + i;
+      return;
+    case K_ZZ1:
+      *dir = (i & 1) ? 2 : 3;
+      *idx = c * (D.d[1] - 1) + i;
+      return;
+    case K_X3:  // dir 0, shape (D0, D1, D2-1), chain c = z*D1 + y
+      *dir = 0;
+      *idx = c * (D.d[2] - 1) + i;
+      return;
+    case K_Y3: {  // dir 1, shape (D0, D1-1, D2), chain c = z*D2 + x
+      *dir = 1;
+      int64_t z = c / D.d[2], x = c % D.d[2];
+      *idx = z * (D.d[1] - 1) * D.d[2] + (int64_t)i * D.d[2] + x;
+      return;
+    }
+    default:  // K_Z3: dir 2, shape (D0-1, D1, D2), chain c = y*D2 + x
+      *dir = 2;
+      *idx = (int64_t)i * D.d[1] * D.d[2] + c;
+      return;
+  }
+}
+
+struct DirPtrs {
+  const double* p[4];
+};
+
+template <class T>
+__global__ void k_build_family_weights(Fam F, Dims D, DirPtrs dw, T* out) {
+  const int64_t total = F.C * (int64_t)(F.m - 1);
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / F.C);
+    const int64_t c = t % F.C;
+    int dir;
+    int64_t idx;
+    fam_edge(F, D, c, i, &dir, &idx);
+    // +0.0 canonicalises -0.0 so a split gate sees the reference's literal 0.0
+    out[t] = (T)(dw.p[dir][idx] + 0.0);
+  }
+}
+
+// ----------------------------------------------------------------- reductions
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum in a fixed order (deterministic); result valid in thread 0.
+__device__ double block_sum(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int k = 0; k < nw; ++k) r += sh[k];
+  }
+  return r;
+}
+
+// out[slot] = sqrt?(sum of parts[0..count)) in index order; one block.
+__global__ void k_reduce_norm(const double* parts, int64_t count, double* out, int do_sqrt) {
+  double acc = 0.0;
+  // each thread sums a contiguous slice; slices combined in thread order
+  const int64_t per = (count + blockDim.x - 1) / blockDim.x;
+  const int64_t lo = threadIdx.x * per, hi = min(count, lo + per);
+  for (int64_t k = lo; k < hi; ++k) acc += parts[k];
+  __shared__ double all[1024];
+  all[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)blockDim.x; ++k) t += all[k];
+    *out = do_sqrt ? sqrt(t) : t;
+  }
+}
+
+// vals[j] = sum over blocks b of parts[b * nv + j]; one block, fixed order.
+__global__ void k_reduce_cols(const double* parts, int nblocks, int nv, double* vals) {
+  const int j = threadIdx.x;
+  if (j >= nv) return;
+  double t = 0.0;
+  for (int b = 0; b < nblocks; ++b) t += parts[(int64_t)b * nv + j];
+  vals[j] = t;
+}
+
+// ----------------------------------------------------------------- accessors
+
+struct AccExact {  // fp64 grid family: y = z - prox(z)
+  const double* z;
+  double* y;
+  const double* wf;
+  Fam F;
+  int64_t c, b;
+  __device__ __forceinline__ double s(int i) const { return z[fam_node(F, b, i)]; }
+  __device__ __forceinline__ double a(int i) const { return wf[(int64_t)i * F.C + c]; }
+  __device__ __forceinline__ void emit(int i, double fill) {
+    const int64_t nd = fam_node(F, b, i);
+    y[nd] = z[nd] - fill;
+  }
+};
+
+struct AccCSR {  // _kernels.prox_chains gather/scatter
+  const double* v;
+  double* out;
+  const int64_t* ids;
+  const double* ew;
+  int proj;
+  __device__ __forceinline__ double s(int i) const { return v[ids[i]]; }
+  __device__ __forceinline__ double a(int i) const { return ew[i]; }
+  __device__ __forceinline__ void emit(int i, double fill) {
+    const int64_t nd = ids[i];
+    out[nd] = proj ? v[nd] - fill : fill;
+  }
+};
+
+struct AccTv1d {  // tv1d_prox on contiguous signals
+  const double* s_;
+  const double* a_;
+  double* x;
+  __device__ __forceinline__ double s(int i) const { return s_[i]; }
+  __device__ __forceinline__ double a(int i) const { return a_[i]; }
+  __device__ __forceinline__ void emit(int i, double fill) { x[i] = fill; }
+};
+
+enum FastRole { R_FIRST = 0, R_MID = 1, R_LAST = 2, R_SHADOW = 3 };
+
+template <int ROLE>
+struct AccFast {  // fp32 state: z_j = p_j + c
+  float* p;
+  double* cdrift;
+  const float* wf;
+  float* G;
+  float* X;
+  double* y;  // R_SHADOW output
+  Fam F;
+  int64_t c, b;
+  double inv_r, rd;
+  double nrm;  // sum of squared step pieces (monitor)
+  __device__ __forceinline__ double s(int i) const {
+    const int64_t nd = fam_node(F, b, i);
+    return (double)p[nd] + cdrift[nd];
+  }
+  __device__ __forceinline__ double a(int i) const { return (double)wf[(int64_t)i * F.C + c]; }
+  __device__ __forceinline__ void emit(int i, double fill) {
+    const int64_t nd = fam_node(F, b, i);
+    const float pold = p[nd];
+    const double cz = cdrift[nd];
+    const double pn = ((double)pold + cz) - fill;
+    if (ROLE == R_SHADOW) {
+      y[nd] = pn;
+      return;
+    }
+    const float p32 = (float)pn;
+    const double d = (double)p32 - (double)pold;
+    p[nd] = p32;
+    nrm += d * d;
+    if (ROLE == R_FIRST) {
+      G[nd] = (float)d;
+    } else if (ROLE == R_MID) {
+      G[nd] = (float)((double)G[nd] + d);
+    } else {
+      const double g = (double)G[nd] + d;
+      const double xn = (double)X[nd] - g;
+      X[nd] = (float)xn;
+      const double dc = (xn - g) * inv_r;
+      cdrift[nd] = cz + dc;
+      nrm += 2.0 * dc * g + rd * dc * dc;
+    }
+  }
+};
+
+// ----------------------------------------------------------------- family kernels
+
+struct Spill {
+  int* cx;
+  double* cy;
+  int* fx;
+  double* fy;
+};
+
+template <class Acc>
+__device__ __forceinline__ void run_chain(Acc& A, int m, const Spill& sp, int64_t gtid,
+                                          int64_t gstride) {
+  __shared__ int s_cx[HC * FAM_BLOCK];
+  __shared__ int s_fx[HC * FAM_BLOCK];
+  __shared__ double s_cy[HC * FAM_BLOCK];
+  __shared__ double s_fy[HC * FAM_BLOCK];
+  pcb::Hull<HC> cH{s_cx + threadIdx.x, s_cy + threadIdx.x, (int)blockDim.x,
+                   sp.cx + gtid, sp.cy + gtid, gstride};
+  pcb::Hull<HC> fH{s_fx + threadIdx.x, s_fy + threadIdx.x, (int)blockDim.x,
+                   sp.fx + gtid, sp.fy + gtid, gstride};
+  pcb::taut_chain(A, cH, fH, m);
+}
+
+__global__ void __launch_bounds__(FAM_BLOCK) k_family_exact(Fam F, const double* z, double* y,
+                                                            const double* wf, Spill sp) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= F.C) return;
+  AccExact A{z, y, wf, F, c, fam_base(F, c)};
+  run_chain(A, F.m, sp, c, (int64_t)gridDim.x * blockDim.x);
+}
+
+template <int ROLE>
+__global__ void __launch_bounds__(FAM_BLOCK) k_family_fast(Fam F, float* p, double* cdrift,
+                                                           const float* wf, float* G, float* X,
+                                                           double* y, double inv_r, double rd,
+                                                           Spill sp, double* parts) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  AccFast<ROLE> A{p, cdrift, wf, G, X, y, F, c, 0, inv_r, rd, 0.0};
+  if (c < F.C) {
+    A.b = fam_base(F, c);
+    run_chain(A, F.m, sp, c, (int64_t)gridDim.x * blockDim.x);
+  }
+  if (ROLE != R_SHADOW) {
+    __shared__ double sh[32];
+    const double t = block_sum(A.nrm, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(FAM_BLOCK) k_prox_csr(const int64_t* node_idx,
+                                                        const int64_t* chain_ptr,
+                                                        const double* edge_w, int64_t c_lo,
+                                                        int64_t c_hi, const double* v, double* out,
+                                                        int proj, Spill sp, const int64_t* soff) {
+  const int64_t c = c_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= c_hi) return;
+  const int64_t b = chain_ptr[c];
+  const int m = (int)(chain_ptr[c + 1] - b);
+  if (m <= 0) return;
+  AccCSR A{v, out, node_idx + b, edge_w + (b - c), proj};
+  // per-chain contiguous spill region (stride 1)
+  __shared__ int s_cx[HC * FAM_BLOCK];
+  __shared__ int s_fx[HC * FAM_BLOCK];
+  __shared__ double s_cy[HC * FAM_BLOCK];
+  __shared__ double s_fy[HC * FAM_BLOCK];
+  const int64_t o = soff[c - c_lo];
+  pcb::Hull<HC> cH{s_cx + threadIdx.x, s_cy + threadIdx.x, (int)blockDim.x, sp.cx + o, sp.cy + o, 1};
+  pcb::Hull<HC> fH{s_fx + threadIdx.x, s_fy + threadIdx.x, (int)blockDim.x, sp.fx + o, sp.fy + o, 1};
+  pcb::taut_chain(A, cH, fH, m);
+}
+
+__global__ void __launch_bounds__(FAM_BLOCK) k_tv1d(const double* s, const double* a,
+                                                    const int64_t* ptr, int64_t nch, double* x,
+                                                    Spill sp, const int64_t* soff) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= nch) return;
+  const int64_t b = ptr[c];
+  const int m = (int)(ptr[c + 1] - b);
+  if (m <= 0) return;
+  AccTv1d A{s + b, a + (b - c), x + b};
+  __shared__ int s_cx[HC * FAM_BLOCK];
+  __shared__ int s_fx[HC * FAM_BLOCK];
+  __shared__ double s_cy[HC * FAM_BLOCK];
+  __shared__ double s_fy[HC * FAM_BLOCK];
+  const int64_t o = soff[c];
+  pcb::Hull<HC> cH{s_cx + threadIdx.x, s_cy + threadIdx.x, (int)blockDim.x, sp.cx + o, sp.cy + o, 1};
+  pcb::Hull<HC> fH{s_fx + threadIdx.x, s_fy + threadIdx.x, (int)blockDim.x, sp.fx + o, sp.fy + o, 1};
+  pcb::taut_chain(A, cH, fH, m);
+}
+
+// ----------------------------------------------------------------- node-wise kernels
+
+// z <- z + ((2y - z) + corr) - y with corr = (w - sum_j (2y_j - z_j)) / r
+// (projections.py:118-122 then solvers.py:295-297, same rounding order).
+template <int R>
+__global__ void k_update_exact(double* z, const double* y, const double* w, int64_t n,
+                               double* parts) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v[R];
+    double total = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      v[j] = 2.0 * y[j * n + i] - z[j * n + i];
+      total = (j == 0) ? v[0] : total + v[j];
+    }
+    const double corr = (w[i] - total) / (double)R;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const double dz = (v[j] + corr) - y[j * n + i];
+      z[j * n + i] = z[j * n + i] + dz;
+      acc += dz * dz;
+    }
+  }
+  __shared__ double sh[32];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+}
+
+// z^0 = Pi_L(0): lam = (0 + (w - 0)/r) * 1 per class.
+__global__ void k_init_exact(double* z, const double* w, int64_t n, int r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double corr = (w[i] - 0.0) / (double)r;
+    for (int j = 0; j < r; ++j) z[j * n + i] = 0.0 + corr;
+  }
+}
+
+// fp32 state from an fp64 z: c = mean_j z_j, p_j = z_j - c, x = w - sum p_j
+__global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, const double* w,
+                           int64_t n, int r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double m = 0.0;
+    for (int j = 0; j < r; ++j) m += z[j * n + i];
+    m /= (double)r;
+    double sp = 0.0;
+    for (int j = 0; j < r; ++j) {
+      const float pj = (float)(z[j * n + i] - m);
+      p[j * n + i] = pj;
+      sp += (double)pj;
+    }
+    cdrift[i] = m;
+    X[i] = (float)(w[i] - sp);
+  }
+}
+
+__global__ void k_init_fast(float* p, double* cdrift, float* X, const double* w, int64_t n, int r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int j = 0; j < r; ++j) p[j * n + i] = 0.0f;
+    cdrift[i] = w[i] / (double)r;
+    X[i] = (float)w[i];
+  }
+}
+
+__global__ void k_get_fast(const float* p, const double* cdrift, double* z, int64_t n, int r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    for (int j = 0; j < r; ++j) z[j * n + i] = (double)p[j * n + i] + cdrift[i];
+  }
+}
+
+// Check-iteration update from the fp64 shadow y (state p^{k-1}, c^{k-1} -> p^k, c^k).
+template <int R>
+__global__ void k_apply_fast(const double* y, float* p, double* cdrift, float* X, const double* w,
+                             int64_t n, double* parts) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double g = 0.0, sp = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const float pn = (float)y[j * n + i];
+      const double d = (double)pn - (double)p[j * n + i];
+      p[j * n + i] = pn;
+      g += d;
+      sp += (double)pn;
+      acc += d * d;
+    }
+    const double xn = w[i] - sp;
+    X[i] = (float)xn;
+    const double dc = (xn - g) / (double)R;
+    cdrift[i] += dc;
+    acc += 2.0 * dc * g + (double)R * dc * dc;
+  }
+  __shared__ double sh[32];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+}
+
+// s = y_0 + y_1 + ... (class order), x = w - s, label bits per threshold,
+// partial sums: [unary_t (T)], dual, ww, dd.
+__global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n, int T,
+                              const double* thr, uint8_t* bits, double* xcur, double* parts) {
+  double un[MAXT];
+  for (int t = 0; t < MAXT; ++t) un[t] = 0.0;
+  double dual = 0.0, ww = 0.0, dd = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = y[i];
+    for (int j = 1; j < r; ++j) s = s + y[(int64_t)j * n + i];
+    const double wi = w[i];
+    const double x = wi - s;
+    xcur[i] = x;
+    unsigned b = 0;
+    for (int t = 0; t < T; ++t) {
+      if (x > thr[t]) {
+        b |= 1u << t;
+        un[t] += wi;
+      }
+    }
+    bits[i] = (uint8_t)b;
+    const double sw = s - wi;
+    dual += fmin(sw, 0.0);
+    ww += wi * wi;
+    dd += sw * sw;
+  }
+  __shared__ double sh[32];
+  const int nv = T + 3;
+  for (int t = 0; t < T; ++t) {
+    const double v = block_sum(un[t], sh);
+    if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + t] = v;
+  }
+  double v = block_sum(dual, sh);
+  if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + T] = v;
+  v = block_sum(ww, sh);
+  if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + T + 1] = v;
+  v = block_sum(dd, sh);
+  if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + T + 2] = v;
+}
+
+struct DirGeom {
+  int ndir;
+  int off[4][3];  // direction offsets (graph.DIRECTIONS)
+};
+
+// cut_t = sum_edges a_e |lab_t(i) - lab_t(j)|, per direction array element.
+__global__ void k_check_edges(Dims D, DirGeom DG, DirPtrs dw, const uint8_t* bits, int T,
+                              double* parts) {
+  double cut[MAXT];
+  for (int t = 0; t < MAXT; ++t) cut[t] = 0.0;
+  int64_t n = 1;
+  for (int a = 0; a < D.nd; ++a) n *= D.d[a];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t co[3];
+    int64_t rem = i;
+    for (int a = D.nd - 1; a >= 0; --a) {
+      co[a] = rem % D.d[a];
+      rem /= D.d[a];
+    }
+    const unsigned bi = bits[i];
+    for (int k = 0; k < DG.ndir; ++k) {
+      // i is the "sa" end of a k-edge iff every coordinate stays in range
+      bool ok = true;
+      int64_t e = 0, j = 0;
+      for (int a = 0; a < D.nd; ++a) {
+        const int o = DG.off[k][a];
+        const int64_t len = D.d[a] - (o < 0 ? -o : o);
+        const int64_t lo = o >= 0 ? 0 : -o;
+        const int64_t q = co[a] - lo;
+        if (q < 0 || q >= len) ok = false;
+        e = e * (len > 0 ? len : 1) + q;
+        j = j * D.d[a] + (co[a] + o);
+      }
+      if (!ok) continue;
+      const double av = dw.p[k][e];
+      const unsigned diff = bi ^ (unsigned)bits[j];
+      for (int t = 0; t < T; ++t)
+        if ((diff >> t) & 1u) cut[t] += av;
+    }
+  }
+  __shared__ double sh[32];
+  for (int t = 0; t < T; ++t) {
+    const double v = block_sum(cut[t], sh);
+    if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * T + t] = v;
+  }
+}
+
+__global__ void k_labels(const uint8_t* bits, int64_t n, int t, uint8_t* lab) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    lab[i] = (bits[i] >> t) & 1u;
+}
+
+// np.packbits order: byte q holds labels 8q..8q+7, label 8q in bit 7.
+__global__ void k_pack(const uint8_t* bits, int64_t n, int t, uint8_t* out) {
+  const int64_t nb = (n + 7) / 8;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nb;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    unsigned v = 0;
+    for (int k = 0; k < 8; ++k) {
+      const int64_t i = q * 8 + k;
+      const unsigned l = i < n ? ((bits[i] >> t) & 1u) : 0u;
+      v |= l << (7 - k);
+    }
+    out[q] = (uint8_t)v;
+  }
+}
+
+__global__ void k_sum_classes(const double* y, int r, int64_t n, double* s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = y[i];
+    for (int j = 1; j < r; ++j) v = v + y[(int64_t)j * n + i];
+    s[i] = v;
+  }
+}
+
+// lam_j = (v_j + corr) * support_j, corr = (w - sum_k v_k) / d on covered nodes.
+__global__ void k_project_L(const double* w, const int64_t* deg, const uint8_t* sup, int r,
+                            int64_t n, const double* v, double* out, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double total = v[i];
+    for (int j = 1; j < r; ++j) total = total + v[(int64_t)j * n + i];
+    double corr = 0.0;
+    if (deg[i] == 0) {
+      if (w[i] != 0.0) atomicExch(bad, 1);
+    } else {
+      corr = (w[i] - total) / (double)deg[i];
+    }
+    for (int j = 0; j < r; ++j) {
+      const int64_t q = (int64_t)j * n + i;
+      out[q] = (v[q] + corr) * (double)sup[q];
+    }
+  }
+}
+
+__global__ void k_diff_norm(const double* a, const double* b, int64_t n, double* parts) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = a[i] - b[i];
+    acc += d * d;
+  }
+  __shared__ double sh[32];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+}
+
+int grid_for(int64_t n, int block, int cap) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+// ----------------------------------------------------------------- device buffers
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    free();
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      p = nullptr;
+      return fail(PCB_E_NOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T),
+                  cudaGetErrorString(e));
+    }
+    n = count;
+    return 0;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { free(); }
+};
+
+}  // namespace
+
+struct pcb_solver {
+  int device = 0;
+  cudaStream_t stream = 0;
+  int precision = PCB_F64;
+  int conn = 0;
+  Dims D{};
+  DirGeom DG{};
+  int r = 0;
+  int64_t n = 0;
+  Fam fam[MAXR]{};
+  int order[MAXR]{};  // fast-mode processing order (last one covers all nodes)
+  int maxm = 1;
+  int64_t maxC = 1;
+  int64_t launches = 0;
+  bool have_state = false;
+  bool have_shadow = false;
+  bool y_valid = false;  // y holds the last shadow (not clobbered by aar_run)
+  bool have_check = false;
+  bool have_best = false;
+  int check_T = 0;
+
+  DBuf<double> w;
+  DBuf<double> dirw[4];
+  DBuf<double> wf64[MAXR];
+  DBuf<float> wf32[MAXR];
+  DBuf<double> z;      // F64: r*n AAR point
+  DBuf<double> y;      // r*n shadow (both modes)
+  DBuf<float> p32;     // F32: r*n shadow state
+  DBuf<double> cdrift; // F32: n drift
+  DBuf<float> X32;     // F32: primal
+  DBuf<float> G32;     // F32: accumulator
+  DBuf<double> tmp;    // r*n scratch (project_K)
+  DBuf<double> yprev;  // r*n previous shadow (dual_tol)
+  DBuf<uint8_t> bits;
+  DBuf<double> xcur;
+  DBuf<uint8_t> bestlab;
+  DBuf<double> bestx;
+  DBuf<double> parts;  // reduction partials
+  DBuf<double> vals;   // reduced values
+  DBuf<double> norms;  // per-iteration step norms
+  DBuf<int> sp_cx, sp_fx;
+  DBuf<double> sp_cy, sp_fy;
+  DBuf<uint8_t> packed;
+  int64_t spill_per = 0;  // spill entries per thread
+  // profiling: event pairs around family launches
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<int> ev_fam;
+  ~pcb_solver() {
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+int set_dev(pcb_solver* h) {
+  CUDA_TRY(cudaSetDevice(h->device));
+  return 0;
+}
+
+// Record an event pair slot around a family launch (profiling only).
+cudaEvent_t prof_event(pcb_solver* h) {
+  if (h->ev_used == h->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    h->ev_pool.push_back(e);
+  }
+  return h->ev_pool[h->ev_used++];
+}
+
+void prof_begin(pcb_solver* h, int fam) {
+  if (!h->profiling) return;
+  cudaEvent_t e = prof_event(h);
+  if (e) {
+    cudaEventRecord(e, h->stream);
+    h->ev_fam.push_back(fam);
+  }
+}
+
+void prof_end(pcb_solver* h) {
+  if (!h->profiling) return;
+  cudaEvent_t e = prof_event(h);
+  if (e) cudaEventRecord(e, h->stream);
+}
+
+Spill spill_of(pcb_solver* h) {
+  return Spill{h->sp_cx.p, h->sp_cy.p, h->sp_fx.p, h->sp_fy.p};
+}
+
+int setup_geometry(pcb_solver* h) {
+  const int64_t* d = h->D.d;
+  auto mk = [](int kind, int m, int64_t C, int64_t cdiv, int64_t chi, int64_t clo, int64_t ns,
+               int64_t zz, int phase) {
+    Fam F;
+    F.kind = kind;
+    F.m = m;
+    F.C = C;
+    F.cdiv = cdiv;
+    F.chi = chi;
+    F.clo = clo;
+    F.ns = ns;
+    F.zz = zz;
+    F.phase = phase;
+    return F;
+  };
+  if (h->conn == PCB_CONN_2D4 || h->conn == PCB_CONN_2D8) {
+    const int64_t H = d[0], W = d[1];
+    h->fam[0] = mk(K_ROW2, (int)W, H, 1, W, 0, 1, 0, 0);
+    h->fam[1] = mk(K_COL2, (int)H, W, 1, 1, 0, W, 0, 0);
+    h->r = 2;
+    if (h->conn == PCB_CONN_2D8) {
+      const int64_t C = (H >= 2 && W >= 2) ? H - 1 : 0;
+      h->fam[2] = mk(K_ZZ0, (int)W, C, 1, W, 0, 1, W, 0);
+      h->fam[3] = mk(K_ZZ1, (int)W, C, 1, W, 0, 1, W, 1);
+      h->r = 4;
+    }
+  } else {
+    const int64_t D0 = d[0], D1 = d[1], D2 = d[2];
+    h->fam[0] = mk(K_X3, (int)D2, D0 * D1, 1, D2, 0, 1, 0, 0);
+    h->fam[1] = mk(K_Y3, (int)D1, D0 * D2, D2, D1 * D2, 1, D2, 0, 0);
+    h->fam[2] = mk(K_Z3, (int)D0, D1 * D2, 1, 1, 0, D1 * D2, 0, 0);
+    h->r = 3;
+  }
+  // fast order: a full-coverage family last (zig-zags leave border singletons)
+  if (h->r == 4) {
+    h->order[0] = 0;
+    h->order[1] = 2;
+    h->order[2] = 3;
+    h->order[3] = 1;
+  } else {
+    for (int j = 0; j < h->r; ++j) h->order[j] = j;
+  }
+  h->maxm = 1;
+  h->maxC = 1;
+  for (int j = 0; j < h->r; ++j) {
+    if (h->fam[j].m > h->maxm) h->maxm = h->fam[j].m;
+    if (h->fam[j].C > h->maxC) h->maxC = h->fam[j].C;
+  }
+  // direction geometry for the certificate kernel
+  static const int off2d4[2][3] = {{0, 1, 0}, {1, 0, 0}};
+  static const int off2d8[4][3] = {{0, 1, 0}, {1, 0, 0}, {1, 1, 0}, {1, -1, 0}};
+  static const int off3d6[3][3] = {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}};
+  if (h->conn == PCB_CONN_2D4) {
+    h->DG.ndir = 2;
+    memcpy(h->DG.off, off2d4, sizeof(off2d4));
+  } else if (h->conn == PCB_CONN_2D8) {
+    h->DG.ndir = 4;
+    memcpy(h->DG.off, off2d8, sizeof(off2d8));
+  } else {
+    h->DG.ndir = 3;
+    memcpy(h->DG.off, off3d6, sizeof(off3d6));
+  }
+  return 0;
+}
+
+int64_t dir_size(const pcb_solver* h, int k) {
+  int64_t s = 1;
+  for (int a = 0; a < h->D.nd; ++a) {
+    int o = h->DG.off[k][a];
+    int64_t len = h->D.d[a] - (o < 0 ? -o : o);
+    s *= len > 0 ? len : 0;
+  }
+  return s;
+}
+
+int ensure_wf64(pcb_solver* h) {
+  DirPtrs dp{};
+  for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
+  for (int j = 0; j < h->r; ++j) {
+    if (h->wf64[j].p) continue;
+    const Fam& F = h->fam[j];
+    const int64_t cnt = F.C * (int64_t)(F.m > 1 ? F.m - 1 : 0);
+    if (int e = h->wf64[j].alloc((size_t)cnt)) return e;
+    if (cnt > 0) {
+      k_build_family_weights<double><<<grid_for(cnt, 256, 148 * 16), 256, 0, h->stream>>>(
+          F, h->D, dp, h->wf64[j].p);
+      LAUNCH_CHECK(h);
+    }
+  }
+  return 0;
+}
+
+int ensure_wf32(pcb_solver* h) {
+  DirPtrs dp{};
+  for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
+  for (int j = 0; j < h->r; ++j) {
+    if (h->wf32[j].p) continue;
+    const Fam& F = h->fam[j];
+    const int64_t cnt = F.C * (int64_t)(F.m > 1 ? F.m - 1 : 0);
+    if (int e = h->wf32[j].alloc((size_t)cnt)) return e;
+    if (cnt > 0) {
+      k_build_family_weights<float><<<grid_for(cnt, 256, 148 * 16), 256, 0, h->stream>>>(
+          F, h->D, dp, h->wf32[j].p);
+      LAUNCH_CHECK(h);
+    }
+  }
+  return 0;
+}
+
+int ensure_spill(pcb_solver* h) {
+  if (h->sp_cx.p) return 0;
+  const int64_t per = h->maxm + 1 > HC ? h->maxm + 1 - HC : 1;
+  const int64_t threads = ((h->maxC + FAM_BLOCK - 1) / FAM_BLOCK) * FAM_BLOCK;
+  const size_t cnt = (size_t)(per * threads);
+  if (int e = h->sp_cx.alloc(cnt)) return e;
+  if (int e = h->sp_fx.alloc(cnt)) return e;
+  if (int e = h->sp_cy.alloc(cnt)) return e;
+  if (int e = h->sp_fy.alloc(cnt)) return e;
+  h->spill_per = per;
+  return 0;
+}
+
+// exact prox of every family: src (r*n) -> dst (r*n)
+int sweep_exact(pcb_solver* h, const double* src, double* dst) {
+  const Spill sp = spill_of(h);
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    if (F.C == 0) continue;
+    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
+    prof_begin(h, j);
+    k_family_exact<<<g, FAM_BLOCK, 0, h->stream>>>(F, src + (int64_t)j * h->n,
+                                                    dst + (int64_t)j * h->n, h->wf64[j].p, sp);
+    prof_end(h);
+    LAUNCH_CHECK(h);
+  }
+  return 0;
+}
+
+constexpr int NODE_GRID = 148 * 8;
+
+int update_exact(pcb_solver* h, double* norm_slot) {
+  const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
+  switch (h->r) {
+    case 2:
+      k_update_exact<2><<<g, RED_BLOCK, 0, h->stream>>>(h->z.p, h->y.p, h->w.p, h->n, h->parts.p);
+      break;
+    case 3:
+      k_update_exact<3><<<g, RED_BLOCK, 0, h->stream>>>(h->z.p, h->y.p, h->w.p, h->n, h->parts.p);
+      break;
+    default:
+      k_update_exact<4><<<g, RED_BLOCK, 0, h->stream>>>(h->z.p, h->y.p, h->w.p, h->n, h->parts.p);
+      break;
+  }
+  LAUNCH_CHECK(h);
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, norm_slot, 1);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+int apply_fast(pcb_solver* h, double* norm_slot) {
+  const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
+  switch (h->r) {
+    case 2:
+      k_apply_fast<2><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+                                                      h->w.p, h->n, h->parts.p);
+      break;
+    case 3:
+      k_apply_fast<3><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+                                                      h->w.p, h->n, h->parts.p);
+      break;
+    default:
+      k_apply_fast<4><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+                                                      h->w.p, h->n, h->parts.p);
+      break;
+  }
+  LAUNCH_CHECK(h);
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, norm_slot, 1);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+// one fused fp32 iteration; partials of every family land in parts[], reduced in order
+int step_fast(pcb_solver* h, double* norm_slot) {
+  const Spill sp = spill_of(h);
+  const double inv_r = 1.0 / (double)h->r, rd = (double)h->r;
+  int64_t off = 0;
+  for (int q = 0; q < h->r; ++q) {
+    const int j = h->order[q];
+    const Fam& F = h->fam[j];
+    const int role = (q == 0) ? R_FIRST : (q == h->r - 1 ? R_LAST : R_MID);
+    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
+    if (F.C == 0) continue;  // only zig-zags can be empty, never first/last
+    float* pj = h->p32.p + (int64_t)j * h->n;
+    double* parts = h->parts.p + off;
+    prof_begin(h, j);
+    if (role == R_FIRST)
+      k_family_fast<R_FIRST><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
+                                                             h->G32.p, h->X32.p, nullptr, inv_r,
+                                                             rd, sp, parts);
+    else if (role == R_MID)
+      k_family_fast<R_MID><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
+                                                           h->G32.p, h->X32.p, nullptr, inv_r, rd,
+                                                           sp, parts);
+    else
+      k_family_fast<R_LAST><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
+                                                            h->G32.p, h->X32.p, nullptr, inv_r,
+                                                            rd, sp, parts);
+    prof_end(h);
+    LAUNCH_CHECK(h);
+    off += g;
+  }
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot, 1);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+int shadow_fast(pcb_solver* h) {
+  const Spill sp = spill_of(h);
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    if (F.C == 0) continue;
+    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
+    k_family_fast<R_SHADOW><<<g, FAM_BLOCK, 0, h->stream>>>(
+        F, h->p32.p + (int64_t)j * h->n, h->cdrift.p, h->wf32[j].p, nullptr, nullptr,
+        h->y.p + (int64_t)j * h->n, 0.0, 0.0, sp, nullptr);
+    LAUNCH_CHECK(h);
+  }
+  return 0;
+}
+
+int parts_needed(const pcb_solver* h) {
+  int64_t fam_blocks = 0;
+  for (int j = 0; j < h->r; ++j) fam_blocks += (h->fam[j].C + FAM_BLOCK - 1) / FAM_BLOCK;
+  int64_t need = fam_blocks;
+  const int64_t node = (int64_t)NODE_GRID * (MAXT + 3);
+  if (node > need) need = node;
+  return (int)need;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* pcb_last_error(void) { return g_err.c_str(); }
+
+int pcb_version(void) { return PCB_VERSION; }
+
+int pcb_device_count(int* count) {
+  if (!count) return fail(PCB_E_ARG, "count is null");
+  CUDA_TRY(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const double* w,
+               const double* const* dir_weights, int device, pcb_solver** out) {
+  if (!out || !dims || !w || !dir_weights) return fail(PCB_E_ARG, "null argument");
+  *out = nullptr;
+  if (conn < 0 || conn > 2) return fail(PCB_E_ARG, "unsupported connectivity code %d", conn);
+  const int want_nd = conn == PCB_CONN_3D6 ? 3 : 2;
+  if (ndim != want_nd) return fail(PCB_E_ARG, "dims rank does not match connectivity");
+  if (precision != PCB_F64 && precision != PCB_F32)
+    return fail(PCB_E_ARG, "unknown precision %d", precision);
+  int64_t n = 1;
+  for (int a = 0; a < ndim; ++a) {
+    if (dims[a] < 1) return fail(PCB_E_ARG, "dims must be positive");
+    if (dims[a] > (int64_t)1 << 30) return fail(PCB_E_ARG, "dimension too large");
+    n *= dims[a];
+  }
+  if (n > ((int64_t)1 << 31) - 1) return fail(PCB_E_ARG, "grid too large for one device (n=%lld)",
+                                              (long long)n);
+  pcb_solver* h = new pcb_solver();
+  h->device = device;
+  h->precision = precision;
+  h->conn = conn;
+  h->D.nd = ndim;
+  h->D.conn = conn;
+  for (int a = 0; a < 3; ++a) h->D.d[a] = a < ndim ? dims[a] : 1;
+  h->n = n;
+  int rc = 0;
+  auto bail = [&](int code) {
+    delete h;
+    return code;
+  };
+  if ((rc = set_dev(h))) return bail(rc);
+  setup_geometry(h);
+  if ((rc = h->w.alloc(n))) return bail(rc);
+  cudaError_t e = cudaMemcpy(h->w.p, w, n * sizeof(double), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "upload w: %s", cudaGetErrorString(e)));
+  for (int k = 0; k < h->DG.ndir; ++k) {
+    const int64_t cnt = dir_size(h, k);
+    if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
+    if (cnt > 0) {
+      if (!dir_weights[k]) return bail(fail(PCB_E_ARG, "direction %d weights are null", k));
+      e = cudaMemcpy(h->dirw[k].p, dir_weights[k], cnt * sizeof(double), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess)
+        return bail(fail(PCB_E_CUDA, "upload weights: %s", cudaGetErrorString(e)));
+    }
+  }
+  const int64_t rn = (int64_t)h->r * n;
+  if ((rc = h->y.alloc(rn))) return bail(rc);
+  e = cudaMemset(h->y.p, 0, rn * sizeof(double));
+  if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "memset: %s", cudaGetErrorString(e)));
+  if (precision == PCB_F64) {
+    if ((rc = h->z.alloc(rn))) return bail(rc);
+    if ((rc = ensure_wf64(h))) return bail(rc);
+  } else {
+    if ((rc = h->p32.alloc(rn))) return bail(rc);
+    if ((rc = h->cdrift.alloc(n))) return bail(rc);
+    if ((rc = h->X32.alloc(n))) return bail(rc);
+    if ((rc = h->G32.alloc(n))) return bail(rc);
+    if ((rc = ensure_wf32(h))) return bail(rc);
+  }
+  if ((rc = ensure_spill(h))) return bail(rc);
+  if ((rc = h->bits.alloc(n))) return bail(rc);
+  if ((rc = h->xcur.alloc(n))) return bail(rc);
+  if ((rc = h->parts.alloc(parts_needed(h)))) return bail(rc);
+  if ((rc = h->vals.alloc(64))) return bail(rc);
+  if ((rc = h->norms.alloc(1))) return bail(rc);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "setup: %s", cudaGetErrorString(e)));
+  *out = h;
+  return 0;
+}
+
+int pcb_destroy(pcb_solver* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  delete h;
+  return 0;
+}
+
+int pcb_shape(const pcb_solver* h, int* r, int64_t* n) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (r) *r = h->r;
+  if (n) *n = h->n;
+  return 0;
+}
+
+int pcb_set_stream(pcb_solver* h, uintptr_t stream) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  h->stream = (cudaStream_t)stream;
+  return 0;
+}
+
+int pcb_synchronize(pcb_solver* h) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (int e = set_dev(h)) return e;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_init_cold(pcb_solver* h) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (int e = set_dev(h)) return e;
+  const int g = grid_for(h->n, 256, NODE_GRID);
+  if (h->precision == PCB_F64) {
+    k_init_exact<<<g, 256, 0, h->stream>>>(h->z.p, h->w.p, h->n, h->r);
+  } else {
+    k_init_fast<<<g, 256, 0, h->stream>>>(h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, h->r);
+  }
+  LAUNCH_CHECK(h);
+  h->have_state = true;
+  h->have_shadow = false;
+  return 0;
+}
+
+int pcb_set_z(pcb_solver* h, const double* z) {
+  if (!h || !z) return fail(PCB_E_ARG, "null argument");
+  if (int e = set_dev(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (h->precision == PCB_F64) {
+    CUDA_TRY(cudaMemcpyAsync(h->z.p, z, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  } else {
+    if (int e = h->tmp.alloc(rn)) return e;
+    CUDA_TRY(cudaMemcpyAsync(h->tmp.p, z, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+        h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, h->r);
+    LAUNCH_CHECK(h);
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->have_state = true;
+  h->have_shadow = false;
+  return 0;
+}
+
+int pcb_get_z(pcb_solver* h, double* z) {
+  if (!h || !z) return fail(PCB_E_ARG, "null argument");
+  if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
+  if (int e = set_dev(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (h->precision == PCB_F64) {
+    CUDA_TRY(cudaMemcpyAsync(z, h->z.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  } else {
+    if (int e = h->tmp.alloc(rn)) return e;
+    k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->p32.p, h->cdrift.p,
+                                                                     h->tmp.p, h->n, h->r);
+    LAUNCH_CHECK(h);
+    CUDA_TRY(cudaMemcpyAsync(z, h->tmp.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_aar_run(pcb_solver* h, int64_t iters, double* step_norms) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
+  if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
+  if (iters == 0) return 0;
+  if (int e = set_dev(h)) return e;
+  if ((int64_t)h->norms.n < iters)
+    if (int e = h->norms.alloc(iters)) return e;
+  for (int64_t k = 0; k < iters; ++k) {
+    int rc;
+    if (h->precision == PCB_F64) {
+      if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
+      if ((rc = update_exact(h, h->norms.p + k))) return rc;
+    } else {
+      if ((rc = step_fast(h, h->norms.p + k))) return rc;
+    }
+  }
+  h->have_shadow = false;
+  h->y_valid = false;
+  if (step_norms) {
+    CUDA_TRY(cudaMemcpyAsync(step_norms, h->norms.p, iters * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  return 0;
+}
+
+int pcb_shadow(pcb_solver* h, double* y_out, double* s_out) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
+  if (int e = set_dev(h)) return e;
+  int rc;
+  if (h->precision == PCB_F64) {
+    if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
+  } else {
+    if ((rc = shadow_fast(h))) return rc;
+  }
+  h->have_shadow = true;
+  h->y_valid = true;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (y_out)
+    CUDA_TRY(cudaMemcpyAsync(y_out, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  if (s_out) {
+    k_sum_classes<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->y.p, h->r, h->n,
+                                                                        h->xcur.p);
+    LAUNCH_CHECK(h);
+    CUDA_TRY(cudaMemcpyAsync(s_out, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+    h->have_check = false;
+  }
+  if (y_out || s_out) CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_shadow_get(pcb_solver* h, double* y_out) {
+  if (!h || !y_out) return fail(PCB_E_ARG, "null argument");
+  if (!h->y_valid) return fail(PCB_E_STATE, "no current shadow");
+  if (int e = set_dev(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  CUDA_TRY(cudaMemcpyAsync(y_out, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_shadow_delta(pcb_solver* h, double* delta) {
+  if (!h || !delta) return fail(PCB_E_ARG, "null argument");
+  if (int e = set_dev(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  const bool had = h->y_valid;
+  if (had) {
+    if (!h->yprev.p)
+      if (int e = h->yprev.alloc(rn)) return e;
+    CUDA_TRY(cudaMemcpyAsync(h->yprev.p, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToDevice,
+                             h->stream));
+  }
+  if (int e = pcb_shadow(h, nullptr, nullptr)) return e;
+  *delta = -1.0;
+  if (had) {
+    const int g = grid_for(rn, RED_BLOCK, NODE_GRID);
+    k_diff_norm<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->yprev.p, rn, h->parts.p);
+    LAUNCH_CHECK(h);
+    k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p, 1);
+    LAUNCH_CHECK(h);
+    CUDA_TRY(cudaMemcpyAsync(delta, h->norms.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  return 0;
+}
+
+int pcb_apply(pcb_solver* h, double* step_norm) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_shadow) return fail(PCB_E_STATE, "apply needs a current shadow (call pcb_shadow)");
+  if (int e = set_dev(h)) return e;
+  int rc;
+  if (h->precision == PCB_F64) {
+    if ((rc = update_exact(h, h->norms.p))) return rc;
+  } else {
+    if ((rc = apply_fast(h, h->norms.p))) return rc;
+  }
+  h->have_shadow = false;
+  if (step_norm) {
+    CUDA_TRY(cudaMemcpyAsync(step_norm, h->norms.p, sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  return 0;
+}
+
+int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double* gap,
+              double* dual_obj) {
+  if (!h || !thr) return fail(PCB_E_ARG, "null argument");
+  if (nthr < 1 || nthr > MAXT) return fail(PCB_E_ARG, "1..%d thresholds supported", MAXT);
+  if (!h->have_shadow) return fail(PCB_E_STATE, "check needs a current shadow (call pcb_shadow)");
+  if (int e = set_dev(h)) return e;
+  // thresholds travel in the tail of vals[]
+  CUDA_TRY(cudaMemcpyAsync(h->vals.p + 48, thr, nthr * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream));
+  const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
+  const int nv = nthr + 3;
+  k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n, nthr, h->vals.p + 48,
+                                                 h->bits.p, h->xcur.p, h->parts.p);
+  LAUNCH_CHECK(h);
+  k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nv, h->vals.p);
+  LAUNCH_CHECK(h);
+  DirPtrs dp{};
+  for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
+  k_check_edges<<<g, RED_BLOCK, 0, h->stream>>>(h->D, h->DG, dp, h->bits.p, nthr, h->parts.p);
+  LAUNCH_CHECK(h);
+  k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nthr, h->vals.p + 16);
+  LAUNCH_CHECK(h);
+  double hv[32];
+  CUDA_TRY(cudaMemcpyAsync(hv, h->vals.p, 32 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  const double dual = hv[nthr];
+  for (int t = 0; t < nthr; ++t) {
+    const double e = hv[16 + t] - hv[t];
+    if (energy) energy[t] = e;
+    if (gap) gap[t] = e - dual;
+  }
+  if (dual_obj) *dual_obj = 0.5 * hv[nthr + 1] - 0.5 * hv[nthr + 2];
+  h->have_check = true;
+  h->check_T = nthr;
+  return 0;
+}
+
+int pcb_get_check(pcb_solver* h, int t, uint8_t* labels, int packed, double* x) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_check) return fail(PCB_E_STATE, "no current check");
+  if (t < 0 || t >= h->check_T) return fail(PCB_E_ARG, "threshold index out of range");
+  if (int e = set_dev(h)) return e;
+  if (labels) {
+    if (packed) {
+      const int64_t nb = (h->n + 7) / 8;
+      if ((int64_t)h->packed.n < nb)
+        if (int e = h->packed.alloc(nb)) return e;
+      k_pack<<<grid_for(nb, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t, h->packed.p);
+      LAUNCH_CHECK(h);
+      CUDA_TRY(cudaMemcpyAsync(labels, h->packed.p, nb, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+      if ((int64_t)h->packed.n < h->n)
+        if (int e = h->packed.alloc(h->n)) return e;
+      k_labels<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t,
+                                                                      h->packed.p);
+      LAUNCH_CHECK(h);
+      CUDA_TRY(cudaMemcpyAsync(labels, h->packed.p, h->n, cudaMemcpyDeviceToHost, h->stream));
+    }
+  }
+  if (x)
+    CUDA_TRY(cudaMemcpyAsync(x, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_keep_best(pcb_solver* h, int t) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_check) return fail(PCB_E_STATE, "no current check");
+  if (t < 0 || t >= h->check_T) return fail(PCB_E_ARG, "threshold index out of range");
+  if (int e = set_dev(h)) return e;
+  if (!h->bestlab.p)
+    if (int e = h->bestlab.alloc(h->n)) return e;
+  if (!h->bestx.p)
+    if (int e = h->bestx.alloc(h->n)) return e;
+  k_labels<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t,
+                                                                  h->bestlab.p);
+  LAUNCH_CHECK(h);
+  CUDA_TRY(cudaMemcpyAsync(h->bestx.p, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToDevice,
+                           h->stream));
+  h->have_best = true;
+  return 0;
+}
+
+int pcb_get_best(pcb_solver* h, uint8_t* labels, double* x) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_best) return fail(PCB_E_STATE, "no best iterate kept");
+  if (int e = set_dev(h)) return e;
+  if (labels)
+    CUDA_TRY(cudaMemcpyAsync(labels, h->bestlab.p, h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (x)
+    CUDA_TRY(cudaMemcpyAsync(x, h->bestx.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_project_K(pcb_solver* h, const double* v, double* out) {
+  if (!h || !v || !out) return fail(PCB_E_ARG, "null argument");
+  if (int e = set_dev(h)) return e;
+  if (int e = ensure_wf64(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if ((int64_t)h->tmp.n < 2 * rn)
+    if (int e = h->tmp.alloc(2 * rn)) return e;
+  double* src = h->tmp.p;
+  double* dst = h->tmp.p + rn;
+  CUDA_TRY(cudaMemcpyAsync(src, v, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaMemsetAsync(dst, 0, rn * sizeof(double), h->stream));
+  if (int e = sweep_exact(h, src, dst)) return e;
+  CUDA_TRY(cudaMemcpyAsync(out, dst, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_set_profiling(pcb_solver* h, int on) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  h->profiling = on != 0;
+  h->ev_used = 0;
+  h->ev_fam.clear();
+  return 0;
+}
+
+int pcb_profile_read(pcb_solver* h, double* ms, int64_t* launches) {
+  if (!h || !ms || !launches) return fail(PCB_E_ARG, "null argument");
+  if (int e = set_dev(h)) return e;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  for (int j = 0; j < h->r; ++j) {
+    ms[j] = 0.0;
+    launches[j] = 0;
+  }
+  for (size_t q = 0; q < h->ev_fam.size(); ++q) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, h->ev_pool[2 * q], h->ev_pool[2 * q + 1]));
+    ms[h->ev_fam[q]] += (double)t;
+    launches[h->ev_fam[q]] += 1;
+  }
+  h->ev_used = 0;
+  h->ev_fam.clear();
+  return 0;
+}
+
+int64_t pcb_launch_count(const pcb_solver* h) { return h ? h->launches : 0; }
+
+void pcb_reset_launch_count(pcb_solver* h) {
+  if (h) h->launches = 0;
+}
+
+// ----------------------------------------------------------------- operator level
+
+int pcb_project_L(const double* w, const int64_t* degree, const uint8_t* support, int r, int64_t n,
+                  const double* v, double* out, int device) {
+  if (!w || !degree || !support || !v || !out) return fail(PCB_E_ARG, "null argument");
+  if (r < 1 || n < 1) return fail(PCB_E_ARG, "empty decomposition");
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t rn = (int64_t)r * n;
+  DBuf<double> d_w, d_v, d_out;
+  DBuf<int64_t> d_deg;
+  DBuf<uint8_t> d_sup;
+  DBuf<int> d_bad;
+  if (int e = d_w.alloc(n)) return e;
+  if (int e = d_v.alloc(rn)) return e;
+  if (int e = d_out.alloc(rn)) return e;
+  if (int e = d_deg.alloc(n)) return e;
+  if (int e = d_sup.alloc(rn)) return e;
+  if (int e = d_bad.alloc(1)) return e;
+  CUDA_TRY(cudaMemcpy(d_w.p, w, n * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_v.p, v, rn * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_deg.p, degree, n * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_sup.p, support, rn, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(d_bad.p, 0, sizeof(int)));
+  k_project_L<<<grid_for(n, 256, NODE_GRID), 256>>>(d_w.p, d_deg.p, d_sup.p, r, n, d_v.p, d_out.p,
+                                                    d_bad.p);
+  LAUNCH_CHECK((pcb_solver*)nullptr);
+  int bad = 0;
+  CUDA_TRY(cudaMemcpy(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) return fail(PCB_E_ARG, "w has mass on coordinates covered by no class");
+  CUDA_TRY(cudaMemcpy(out, d_out.p, rn * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+static int csr_spill(int64_t nch, const int64_t* lens_host, DBuf<int64_t>& soff, DBuf<int>& cx,
+                     DBuf<double>& cy, DBuf<int>& fx, DBuf<double>& fy) {
+  std::vector<int64_t> off(nch > 0 ? nch : 1);
+  int64_t tot = 0;
+  for (int64_t c = 0; c < nch; ++c) {
+    off[c] = tot;
+    const int64_t need = lens_host[c] + 1 - HC;
+    tot += need > 0 ? need : 0;
+  }
+  if (tot == 0) tot = 1;
+  if (int e = soff.alloc(off.size())) return e;
+  CUDA_TRY(cudaMemcpy(soff.p, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (int e = cx.alloc(tot)) return e;
+  if (int e = fx.alloc(tot)) return e;
+  if (int e = cy.alloc(tot)) return e;
+  if (int e = fy.alloc(tot)) return e;
+  return 0;
+}
+
+int pcb_prox_chains(const int64_t* node_idx, const int64_t* chain_ptr, const double* edge_w,
+                    int64_t c_lo, int64_t c_hi, int64_t n_nodes, int64_t n_idx, int64_t n_edges,
+                    const double* v, double* out, int as_projection, int device) {
+  if (!node_idx || !chain_ptr || !v || !out) return fail(PCB_E_ARG, "null argument");
+  if (c_lo < 0 || c_hi < c_lo) return fail(PCB_E_ARG, "bad chain range");
+  if (c_hi == c_lo) return 0;
+  CUDA_TRY(cudaSetDevice(device));
+  const int64_t nch = c_hi - c_lo;
+  std::vector<int64_t> lens(nch);
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t m = chain_ptr[c_lo + c + 1] - chain_ptr[c_lo + c];
+    if (m < 0 || chain_ptr[c_lo + c + 1] > n_idx)
+      return fail(PCB_E_ARG, "chain_ptr out of range");
+    lens[c] = m;
+  }
+  DBuf<int64_t> d_idx, d_ptr, soff;
+  DBuf<double> d_ew, d_v, d_out, cy, fy;
+  DBuf<int> cx, fx;
+  if (int e = d_idx.alloc(n_idx)) return e;
+  if (int e = d_ptr.alloc(c_hi + 1)) return e;
+  if (int e = d_ew.alloc(n_edges)) return e;
+  if (int e = d_v.alloc(n_nodes)) return e;
+  if (int e = d_out.alloc(n_nodes)) return e;
+  CUDA_TRY(cudaMemcpy(d_idx.p, node_idx, n_idx * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_ptr.p, chain_ptr, (c_hi + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  if (n_edges > 0 && edge_w)
+    CUDA_TRY(cudaMemcpy(d_ew.p, edge_w, n_edges * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_v.p, v, n_nodes * sizeof(double), cudaMemcpyHostToDevice));
+  // out is updated only on chain nodes: start from the caller's contents
+  CUDA_TRY(cudaMemcpy(d_out.p, out, n_nodes * sizeof(double), cudaMemcpyHostToDevice));
+  if (int e = csr_spill(nch, lens.data(), soff, cx, cy, fx, fy)) return e;
+  Spill sp{cx.p, cy.p, fx.p, fy.p};
+  const int g = (int)((nch + FAM_BLOCK - 1) / FAM_BLOCK);
+  k_prox_csr<<<g, FAM_BLOCK>>>(d_idx.p, d_ptr.p, d_ew.p, c_lo, c_hi, d_v.p, d_out.p,
+                               as_projection ? 1 : 0, sp, soff.p);
+  LAUNCH_CHECK((pcb_solver*)nullptr);
+  CUDA_TRY(cudaMemcpy(out, d_out.p, n_nodes * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int pcb_tv1d_prox_batch(const double* s, const double* a, const int64_t* ptr, int64_t nchains,
+                        double* x, int device) {
+  if (!s || !ptr || !x) return fail(PCB_E_ARG, "null argument");
+  if (nchains <= 0) return 0;
+  CUDA_TRY(cudaSetDevice(device));
+  std::vector<int64_t> lens(nchains);
+  const int64_t total = ptr[nchains];
+  for (int64_t c = 0; c < nchains; ++c) {
+    lens[c] = ptr[c + 1] - ptr[c];
+    if (lens[c] < 1) return fail(PCB_E_ARG, "empty signal in batch");
+  }
+  const int64_t nedge = total - nchains;
+  DBuf<int64_t> d_ptr, soff;
+  DBuf<double> d_s, d_a, d_x, cy, fy;
+  DBuf<int> cx, fx;
+  if (int e = d_ptr.alloc(nchains + 1)) return e;
+  if (int e = d_s.alloc(total)) return e;
+  if (int e = d_a.alloc(nedge)) return e;
+  if (int e = d_x.alloc(total)) return e;
+  CUDA_TRY(cudaMemcpy(d_ptr.p, ptr, (nchains + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(d_s.p, s, total * sizeof(double), cudaMemcpyHostToDevice));
+  if (nedge > 0 && a) CUDA_TRY(cudaMemcpy(d_a.p, a, nedge * sizeof(double), cudaMemcpyHostToDevice));
+  if (int e = csr_spill(nchains, lens.data(), soff, cx, cy, fx, fy)) return e;
+  Spill sp{cx.p, cy.p, fx.p, fy.p};
+  const int g = (int)((nchains + FAM_BLOCK - 1) / FAM_BLOCK);
+  k_tv1d<<<g, FAM_BLOCK>>>(d_s.p, d_a.p, d_ptr.p, nchains, d_x.p, sp, soff.p);
+  LAUNCH_CHECK((pcb_solver*)nullptr);
+  CUDA_TRY(cudaMemcpy(x, d_x.p, total * sizeof(double), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+}  // extern "C"

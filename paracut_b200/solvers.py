@@ -1,0 +1,309 @@
+"""AAR solver driver on the B200 path (reference solvers.py surface).
+
+``solve(g, dec, cfg)`` / ``solve_aar`` keep the reference's configuration,
+result, trace, best-iterate, stopping and warm-start semantics
+(solvers.py:33-209, 272-307); every iteration runs on the device:
+
+* plain iterations between checks: ``pcb_aar_run`` (fused prox sweeps plus
+  the reflect/average update, step norms accumulated on the device);
+* check iterations: ``pcb_shadow`` (y = Pi_K(z)), ``pcb_check`` (threshold,
+  cut, unary and dual reductions for up to 8 thresholds in one pass), then
+  ``pcb_apply`` (z update from that shadow) if the loop continues.
+
+Precision: ``SolverConfig.precision="f64"`` (default) keeps z in fp64 and
+reproduces the reference iterates bit for bit; ``"f32"`` stores the bounded
+shadows in fp32 with an fp64 drift vector (SURVEY 8(a) a6 fused form) and
+computes every prox in fp64 -- the fast path for large grids.
+
+Extensions (defaults give the reference's behaviour): ``thresholds`` lists
+extra primal thresholds evaluated in the same pass; each check keeps the
+smallest-gap one (ties -> earlier entry), which certifies integer instances
+with exact-zero plateaus.  The algorithms "bcd", "ap" and
+"fista" are accepted by ``SolverConfig`` for compatibility but are outside
+this path and raise NotImplementedError in ``solve``.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .certify import jaccard_distance, jaccard_packed
+from .decompose import ChainDecomposition, GridDecomposition
+from .graph import as_grid, instance_fingerprint
+from .projections import DualState
+
+ALGORITHMS = ("bcd", "ap", "aar", "fista")
+GAP_SLACK = 1e-6
+PRECISIONS = ("f64", "f32")
+MAX_THRESHOLDS = 8
+
+
+@dataclass
+class SolverConfig:
+    algorithm: str = "aar"
+    max_iters: int = 20000
+    gap_tol: float = 0.0
+    dual_tol: float = 0.0
+    threads: int = 1
+    check_every: int = 10
+    warm_start: DualState | None = None
+    force_warm: bool = False
+    reference: np.ndarray | None = None
+    # --- B200 extensions
+    precision: str = "f64"
+    thresholds: tuple = (0.0,)
+    device: int = 0
+
+    def __post_init__(self):
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError("unknown algorithm %r" % (self.algorithm,))
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.gap_tol < 0 or self.dual_tol < 0:
+            raise ValueError("tolerances must be >= 0")
+        if self.threads < 1 or self.check_every < 1:
+            raise ValueError("threads and check_every must be >= 1")
+        if self.precision not in PRECISIONS:
+            raise ValueError("precision must be one of %r" % (PRECISIONS,))
+        thr = tuple(float(t) for t in self.thresholds)
+        if not 1 <= len(thr) <= MAX_THRESHOLDS:
+            raise ValueError("1..%d thresholds supported" % MAX_THRESHOLDS)
+        self.thresholds = thr
+
+
+@dataclass
+class TraceRow:
+    iteration: int
+    gap: float
+    dual_objective: float
+    energy: float
+    jaccard: float
+    wall_s: float
+
+
+@dataclass
+class SolveResult:
+    labeling: np.ndarray
+    tv_solution: np.ndarray
+    energy: float
+    gap: float
+    iterations: int
+    certified: bool
+    dual_state: DualState
+    trace: list
+    wall_time: float
+    algorithm: str
+    monitor: dict = field(default_factory=dict)
+    threshold: float = 0.0   # primal threshold of the reported labeling (extension)
+
+
+def threshold(x):
+    """x_i > 0 -> 1, else 0 (strict; solvers.py:81-83)."""
+    return (np.asarray(x) > 0).astype(np.uint8)
+
+
+def level_sets(x):
+    """Nested labelings thresholding x above each of its values (solvers.py:86-97)."""
+    x = np.asarray(x, dtype=np.float64)
+    labs = [np.ones(x.size, dtype=np.uint8)]
+    for v in np.unique(x):
+        labs.append((x > v).astype(np.uint8))
+    return labs
+
+
+class _DeviceDualState(DualState):
+    """DualState whose y/z stay on the device until first read."""
+
+    def __init__(self, solver, g):
+        self._solver = solver
+        self._g = g
+        self._y = self._z = self._fp = None
+        self.lam = None
+
+    def _fetch(self):
+        if self._solver is not None:
+            self._y = self._solver.shadow_get()
+            self._z = self._solver.get_z()
+            self._solver = None
+
+    @property
+    def y(self):
+        self._fetch()
+        return self._y
+
+    @y.setter
+    def y(self, v):
+        self._fetch()
+        self._y = v
+
+    @property
+    def z(self):
+        self._fetch()
+        return self._z
+
+    @z.setter
+    def z(self, v):
+        self._fetch()
+        self._z = v
+
+    @property
+    def fingerprint(self):
+        if self._fp is None and self._g is not None:
+            self._fp = instance_fingerprint(self._g)
+        return self._fp
+
+    @fingerprint.setter
+    def fingerprint(self, v):
+        self._fp = v
+        self._g = None
+
+
+class _Driver:
+    """Per-solve bookkeeping mirroring solvers.py:124-209."""
+
+    def __init__(self, g, dec, cfg):
+        if not isinstance(dec, (GridDecomposition, ChainDecomposition)) or dec.n != g.n:
+            raise ValueError("decomposition does not match the instance")
+        if not isinstance(dec, GridDecomposition):
+            raise ValueError("the B200 solver needs a grid decomposition (decompose_grid)")
+        self.g = g
+        self.cfg = cfg
+        self.r = dec.r
+        self.shape = (dec.r, g.n)
+        self.trace = []
+        self.monitor = {}
+        self.best_gap = np.inf
+        self.best_energy = np.nan
+        self.best_t = 0
+        self.best_packed = None
+        self.iterations = 0
+        self.stopped = False
+        self._labs = []
+        self.thr = np.asarray(cfg.thresholds, dtype=np.float64)
+        self.solver = _native.GridSolver(g, precision=cfg.precision, device=cfg.device)
+        self.t0 = time.perf_counter()
+
+    def warm_or_cold(self):
+        ws = self.cfg.warm_start
+        if ws is None:
+            self.solver.init_cold()
+            return
+        fp = instance_fingerprint(self.g)
+        if ws.fingerprint is not None and ws.fingerprint != fp and not self.cfg.force_warm:
+            raise ValueError("warm start fingerprint does not match instance")
+        for name in ("z", "y"):
+            v = getattr(ws, name, None)
+            if v is not None:
+                if v.shape != self.shape:
+                    raise ValueError("warm start shape %r, expected %r" % (v.shape, self.shape))
+                self.solver.set_z(np.asarray(v, dtype=np.float64))
+                return
+        self.solver.init_cold()
+
+    def record(self, name, values):
+        self.monitor.setdefault(name, []).extend(float(v) for v in np.atleast_1d(values))
+
+    def check(self, k):
+        energies, gaps, dual = self.solver.check(self.thr)
+        t = int(np.argmin(gaps))  # first minimum: threshold 0 wins ties
+        gap, en = float(gaps[t]), float(energies[t])
+        jac = np.nan
+        packed = None
+        if self.cfg.reference is not None:
+            lab = self.solver.check_labels(t)
+            jac = jaccard_distance(lab, self.cfg.reference)
+        else:
+            packed = self.solver.check_labels(t, packed=True)
+            self._labs.append(packed)
+        self.trace.append(TraceRow(k, gap, dual, en, jac, time.perf_counter() - self.t0))
+        if gap < self.best_gap:
+            self.best_gap = gap
+            self.best_energy = en
+            self.best_t = t
+            self.best_packed = packed
+            self.solver.keep_best(t)
+        self.iterations = k
+        if gap <= self.cfg.gap_tol + GAP_SLACK:
+            self.stopped = True
+        return self.stopped
+
+    def due(self, k):
+        return k % self.cfg.check_every == 0 or k >= self.cfg.max_iters
+
+    def next_due(self, k):
+        ce = self.cfg.check_every
+        return min(((k // ce) + 1) * ce, self.cfg.max_iters)
+
+    def finish(self):
+        wall = time.perf_counter() - self.t0
+        lab, x = self.solver.get_best()
+        certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
+        if self.cfg.reference is None:
+            for row, packed in zip(self.trace, self._labs):
+                row.jaccard = jaccard_packed(packed, self.best_packed)
+        state = _DeviceDualState(self.solver, self.g)
+        return SolveResult(labeling=lab, tv_solution=x, energy=self.best_energy,
+                           gap=self.best_gap, iterations=self.iterations, certified=certified,
+                           dual_state=state, trace=self.trace, wall_time=wall,
+                           algorithm=self.cfg.algorithm, monitor=self.monitor,
+                           threshold=float(self.thr[self.best_t]))
+
+
+def solve_aar(g, dec, cfg):
+    """Averaged alternating reflections on the device (solvers.py:272-307)."""
+    g = as_grid(g)
+    drv = _Driver(g, dec, cfg)
+    drv.warm_or_cold()
+    S = drv.solver
+    k = 0
+    if cfg.dual_tol > 0:
+        have_prev = False
+        while True:
+            delta = S.shadow_delta()
+            if drv.due(k) and drv.check(k):
+                break
+            if k >= cfg.max_iters:
+                break
+            drv.record("aar_step_norm", S.apply())
+            k += 1
+            if have_prev and delta <= cfg.dual_tol:
+                S.shadow()
+                drv.check(k)
+                break
+            have_prev = True
+        return drv.finish()
+    while True:
+        if drv.due(k):
+            S.shadow()
+            if drv.check(k) or k >= cfg.max_iters:
+                break
+            drv.record("aar_step_norm", S.apply())
+            k += 1
+        else:
+            nxt = drv.next_due(k)
+            drv.record("aar_step_norm", S.run(nxt - k))
+            k = nxt
+    return drv.finish()
+
+
+def _not_on_path(name):
+    def run(g, dec, cfg):
+        raise NotImplementedError(
+            "algorithm %r is outside the B200 hot path (only 'aar' runs on the device; "
+            "BCD/AP/FISTA are SURVEY 8(f) rank 2)" % name)
+    return run
+
+
+solve_bcd = _not_on_path("bcd")
+solve_ap = _not_on_path("ap")
+solve_fista = _not_on_path("fista")
+
+_SOLVERS = {"bcd": solve_bcd, "ap": solve_ap, "aar": solve_aar, "fista": solve_fista}
+
+
+def solve(g, dec, cfg):
+    """Dispatch on cfg.algorithm (solvers.py:348-350)."""
+    return _SOLVERS[cfg.algorithm](g, dec, cfg)
