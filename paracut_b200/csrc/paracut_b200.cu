@@ -12,8 +12,9 @@
 //                    (projections.py:89-104 / _kernels.py:145-180)
 //   k_update_exact   z += Pi_L(2y - z) - y in the reference's operation order
 //                    (solvers.py:295-298, projections.py:107-122)
-//   k_family_fast    fused fp32-state sweep: prox of z_j = p_j + c, p_j in
-//                    place, accumulator G, last family applies the drift update
+//   fast::k_sweep    staged fp32-state sweep (fast_sweep.cuh): prox of
+//                    z_j = p_j + c, p_j in place, accumulator G, the last
+//                    family applies the drift/primal update
 //   k_apply_fast     check-iteration update from an fp64 shadow
 //   k_check_nodes / k_check_edges   threshold, unary, dual, cut partials
 //   k_reduce_*       deterministic fixed-order final reductions
@@ -133,6 +134,57 @@ __device__ __forceinline__ void fam_edge(const Fam& F, const Dims& D, int64_t c,
   }
 }
 
+// Inverse of fam_node: chain and position of grid node nd in family F
+// (false for the border nodes a zig-zag family leaves as singletons).
+__device__ __forceinline__ bool fam_index(const Fam& F, const Dims& D, int64_t nd, int64_t* c,
+                                          int* i) {
+  switch (F.kind) {
+    case K_ROW2:
+      *c = nd / D.d[1];
+      *i = (int)(nd % D.d[1]);
+      return true;
+    case K_COL2:
+      *c = nd % D.d[1];
+      *i = (int)(nd / D.d[1]);
+      return true;
+    case K_ZZ0:
+    case K_ZZ1: {
+      const int64_t y = nd / D.d[1], x = nd % D.d[1];
+      const int64_t r = y - ((x + F.phase) & 1);
+      if (r < 0 || r >= F.C) return false;
+      *c = r;
+      *i = (int)x;
+      return true;
+    }
+    case K_X3:
+      *c = nd / D.d[2];
+      *i = (int)(nd % D.d[2]);
+      return true;
+    case K_Y3: {
+      const int64_t plane = D.d[1] * D.d[2];
+      const int64_t z = nd / plane, rem = nd % plane;
+      *c = z * D.d[2] + rem % D.d[2];
+      *i = (int)(rem / D.d[2]);
+      return true;
+    }
+    default: {
+      const int64_t plane = D.d[1] * D.d[2];
+      *c = nd % plane;
+      *i = (int)(nd / plane);
+      return true;
+    }
+  }
+}
+
+__host__ __device__ inline bool fam_rowlike(int kind) {
+  return kind == K_ROW2 || kind == K_ZZ0 || kind == K_ZZ1 || kind == K_X3;
+}
+
+struct FamSet {
+  Fam f[MAXR];
+  int r;
+};
+
 struct DirPtrs {
   const double* p[4];
 };
@@ -240,53 +292,6 @@ struct AccTv1d {  // tv1d_prox on contiguous signals
   __device__ __forceinline__ void emit(int i, double fill) { x[i] = fill; }
 };
 
-enum FastRole { R_FIRST = 0, R_MID = 1, R_LAST = 2, R_SHADOW = 3 };
-
-template <int ROLE>
-struct AccFast {  // fp32 state: z_j = p_j + c
-  float* p;
-  double* cdrift;
-  const float* wf;
-  float* G;
-  float* X;
-  double* y;  // R_SHADOW output
-  Fam F;
-  int64_t c, b;
-  double inv_r, rd;
-  double nrm;  // sum of squared step pieces (monitor)
-  __device__ __forceinline__ double s(int i) const {
-    const int64_t nd = fam_node(F, b, i);
-    return (double)p[nd] + cdrift[nd];
-  }
-  __device__ __forceinline__ double a(int i) const { return (double)wf[(int64_t)i * F.C + c]; }
-  __device__ __forceinline__ void emit(int i, double fill) {
-    const int64_t nd = fam_node(F, b, i);
-    const float pold = p[nd];
-    const double cz = cdrift[nd];
-    const double pn = ((double)pold + cz) - fill;
-    if (ROLE == R_SHADOW) {
-      y[nd] = pn;
-      return;
-    }
-    const float p32 = (float)pn;
-    const double d = (double)p32 - (double)pold;
-    p[nd] = p32;
-    nrm += d * d;
-    if (ROLE == R_FIRST) {
-      G[nd] = (float)d;
-    } else if (ROLE == R_MID) {
-      G[nd] = (float)((double)G[nd] + d);
-    } else {
-      const double g = (double)G[nd] + d;
-      const double xn = (double)X[nd] - g;
-      X[nd] = (float)xn;
-      const double dc = (xn - g) * inv_r;
-      cdrift[nd] = cz + dc;
-      nrm += 2.0 * dc * g + rd * dc * dc;
-    }
-  }
-};
-
 // ----------------------------------------------------------------- family kernels
 
 struct Spill {
@@ -316,24 +321,6 @@ __global__ void __launch_bounds__(FAM_BLOCK) k_family_exact(Fam F, const double*
   if (c >= F.C) return;
   AccExact A{z, y, wf, F, c, fam_base(F, c)};
   run_chain(A, F.m, sp, c, (int64_t)gridDim.x * blockDim.x);
-}
-
-template <int ROLE>
-__global__ void __launch_bounds__(FAM_BLOCK) k_family_fast(Fam F, float* p, double* cdrift,
-                                                           const float* wf, float* G, float* X,
-                                                           double* y, double inv_r, double rd,
-                                                           Spill sp, double* parts) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  AccFast<ROLE> A{p, cdrift, wf, G, X, y, F, c, 0, inv_r, rd, 0.0};
-  if (c < F.C) {
-    A.b = fam_base(F, c);
-    run_chain(A, F.m, sp, c, (int64_t)gridDim.x * blockDim.x);
-  }
-  if (ROLE != R_SHADOW) {
-    __shared__ double sh[32];
-    const double t = block_sum(A.nrm, sh);
-    if (threadIdx.x == 0) parts[blockIdx.x] = t;
-  }
 }
 
 __global__ void __launch_bounds__(FAM_BLOCK) k_prox_csr(const int64_t* node_idx,
@@ -377,6 +364,12 @@ __global__ void __launch_bounds__(FAM_BLOCK) k_tv1d(const double* s, const doubl
   pcb::taut_chain(A, cH, fH, m);
 }
 
+}  // namespace
+
+#include "fast_sweep.cuh"
+
+namespace {
+
 // ----------------------------------------------------------------- node-wise kernels
 
 // z <- z + ((2y - z) + corr) - y with corr = (w - sum_j (2y_j - z_j)) / r
@@ -416,9 +409,11 @@ __global__ void k_init_exact(double* z, const double* w, int64_t n, int r) {
   }
 }
 
-// fp32 state from an fp64 z: c = mean_j z_j, p_j = z_j - c, x = w - sum p_j
+// fp32 state from an fp64 z (natural [j][node]): c = mean_j z_j, p_j = z_j - c
+// stored chain-interleaved, x = w - sum_j p_j.
 __global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, const double* w,
-                           int64_t n, int r) {
+                           int64_t n, FamSet FS, Dims D) {
+  const int r = FS.r;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double m = 0.0;
@@ -426,8 +421,11 @@ __global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, 
     m /= (double)r;
     double sp = 0.0;
     for (int j = 0; j < r; ++j) {
+      int64_t c;
+      int pos;
+      if (!fam_index(FS.f[j], D, i, &c, &pos)) continue;  // zig-zag border: p = 0
       const float pj = (float)(z[j * n + i] - m);
-      p[j * n + i] = pj;
+      p[j * n + (int64_t)pos * FS.f[j].C + c] = pj;
       sp += (double)pj;
     }
     cdrift[i] = m;
@@ -444,26 +442,37 @@ __global__ void k_init_fast(float* p, double* cdrift, float* X, const double* w,
   }
 }
 
-__global__ void k_get_fast(const float* p, const double* cdrift, double* z, int64_t n, int r) {
+__global__ void k_get_fast(const float* p, const double* cdrift, double* z, int64_t n, FamSet FS,
+                           Dims D) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    for (int j = 0; j < r; ++j) z[j * n + i] = (double)p[j * n + i] + cdrift[i];
+    for (int j = 0; j < FS.r; ++j) {
+      int64_t c;
+      int pos;
+      const float pj = fam_index(FS.f[j], D, i, &c, &pos)
+                           ? p[j * n + (int64_t)pos * FS.f[j].C + c] : 0.0f;
+      z[j * n + i] = (double)pj + cdrift[i];
+    }
   }
 }
 
 // Check-iteration update from the fp64 shadow y (state p^{k-1}, c^{k-1} -> p^k, c^k).
 template <int R>
 __global__ void k_apply_fast(const double* y, float* p, double* cdrift, float* X, const double* w,
-                             int64_t n, double* parts) {
+                             int64_t n, FamSet FS, Dims D, double* parts) {
   double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double g = 0.0, sp = 0.0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
+      int64_t c;
+      int pos;
+      if (!fam_index(FS.f[j], D, i, &c, &pos)) continue;
+      const int64_t q = j * n + (int64_t)pos * FS.f[j].C + c;
       const float pn = (float)y[j * n + i];
-      const double d = (double)pn - (double)p[j * n + i];
-      p[j * n + i] = pn;
+      const double d = (double)pn - (double)p[q];
+      p[q] = pn;
       g += d;
       sp += (double)pn;
       acc += d * d;
@@ -752,6 +761,13 @@ void prof_end(pcb_solver* h) {
   if (e) cudaEventRecord(e, h->stream);
 }
 
+FamSet famset(const pcb_solver* h) {
+  FamSet FS{};
+  FS.r = h->r;
+  for (int j = 0; j < h->r; ++j) FS.f[j] = h->fam[j];
+  return FS;
+}
+
 Spill spill_of(pcb_solver* h) {
   return Spill{h->sp_cx.p, h->sp_cy.p, h->sp_fx.p, h->sp_fy.p};
 }
@@ -921,15 +937,15 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   switch (h->r) {
     case 2:
       k_apply_fast<2><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
-                                                      h->w.p, h->n, h->parts.p);
+                                                      h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
     case 3:
       k_apply_fast<3><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
-                                                      h->w.p, h->n, h->parts.p);
+                                                      h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
     default:
       k_apply_fast<4><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
-                                                      h->w.p, h->n, h->parts.p);
+                                                      h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
   }
   LAUNCH_CHECK(h);
@@ -938,34 +954,43 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
+template <int ROLE, bool ROWLIKE>
+int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
+  const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>();
+  CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  const int per = pcb::fast::WARPS * 32;
+  const int g = (int)((a.F.C + per - 1) / per);
+  pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+template <int ROLE>
+int launch_role(pcb_solver* h, const pcb::fast::Args& a) {
+  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a) : launch_sweep<ROLE, false>(h, a);
+}
+
 // one fused fp32 iteration; partials of every family land in parts[], reduced in order
 int step_fast(pcb_solver* h, double* norm_slot) {
-  const Spill sp = spill_of(h);
   const double inv_r = 1.0 / (double)h->r, rd = (double)h->r;
   int64_t off = 0;
   for (int q = 0; q < h->r; ++q) {
     const int j = h->order[q];
     const Fam& F = h->fam[j];
-    const int role = (q == 0) ? R_FIRST : (q == h->r - 1 ? R_LAST : R_MID);
-    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
     if (F.C == 0) continue;  // only zig-zags can be empty, never first/last
-    float* pj = h->p32.p + (int64_t)j * h->n;
-    double* parts = h->parts.p + off;
+    const int role = (q == 0) ? pcb::fast::FIRST : (q == h->r - 1 ? pcb::fast::LAST
+                                                                   : pcb::fast::MID);
+    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
+    pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
+                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off};
     prof_begin(h, j);
-    if (role == R_FIRST)
-      k_family_fast<R_FIRST><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
-                                                             h->G32.p, h->X32.p, nullptr, inv_r,
-                                                             rd, sp, parts);
-    else if (role == R_MID)
-      k_family_fast<R_MID><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
-                                                           h->G32.p, h->X32.p, nullptr, inv_r, rd,
-                                                           sp, parts);
-    else
-      k_family_fast<R_LAST><<<g, FAM_BLOCK, 0, h->stream>>>(F, pj, h->cdrift.p, h->wf32[j].p,
-                                                            h->G32.p, h->X32.p, nullptr, inv_r,
-                                                            rd, sp, parts);
+    int rc;
+    if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a);
+    else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a);
+    else rc = launch_sweep<pcb::fast::LAST, false>(h, a);
     prof_end(h);
-    LAUNCH_CHECK(h);
+    if (rc) return rc;
     off += g;
   }
   k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot, 1);
@@ -974,15 +999,12 @@ int step_fast(pcb_solver* h, double* norm_slot) {
 }
 
 int shadow_fast(pcb_solver* h) {
-  const Spill sp = spill_of(h);
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
     if (F.C == 0) continue;
-    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
-    k_family_fast<R_SHADOW><<<g, FAM_BLOCK, 0, h->stream>>>(
-        F, h->p32.p + (int64_t)j * h->n, h->cdrift.p, h->wf32[j].p, nullptr, nullptr,
-        h->y.p + (int64_t)j * h->n, 0.0, 0.0, sp, nullptr);
-    LAUNCH_CHECK(h);
+    pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
+                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, nullptr};
+    if (int rc = launch_role<pcb::fast::SHADOW>(h, a)) return rc;
   }
   return 0;
 }
@@ -1136,7 +1158,7 @@ int pcb_set_z(pcb_solver* h, const double* z) {
     if (int e = h->tmp.alloc(rn)) return e;
     CUDA_TRY(cudaMemcpyAsync(h->tmp.p, z, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
     k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
-        h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, h->r);
+        h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, famset(h), h->D);
     LAUNCH_CHECK(h);
   }
   CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1155,7 +1177,8 @@ int pcb_get_z(pcb_solver* h, double* z) {
   } else {
     if (int e = h->tmp.alloc(rn)) return e;
     k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->p32.p, h->cdrift.p,
-                                                                     h->tmp.p, h->n, h->r);
+                                                                     h->tmp.p, h->n, famset(h),
+                                                                     h->D);
     LAUNCH_CHECK(h);
     CUDA_TRY(cudaMemcpyAsync(z, h->tmp.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   }

@@ -61,3 +61,59 @@ def test_full_size_cfg4_f64_bitwise_vs_oracle():
                    pc.SolverConfig(max_iters=k, check_every=k + 1, precision="f64"))
     assert np.array_equal(res.dual_state.z, z_ref)
     assert np.array_equal(res.dual_state.y, y_ref)
+
+
+def _weights_regime(rng, shapes, regime):
+    out = []
+    for s in shapes:
+        if regime == "uniform":
+            a = rng.uniform(0, 2, s)
+        elif regime == "huge":
+            a = rng.uniform(20, 80, s)
+        elif regime == "zeros":
+            a = rng.integers(0, 3, s).astype(float)
+        else:
+            a = np.abs(rng.normal(0, 0.5, s))
+        out.append(a)
+    return out
+
+
+@pytest.mark.parametrize("regime", ["uniform", "huge", "zeros", "critical"])
+@pytest.mark.parametrize("conn,dims", [("2D-4", (37, 290)), ("2D-8", (41, 75)),
+                                       ("3D-6", (9, 70, 45)), ("2D-4", (1, 100)),
+                                       ("3D-6", (130, 3, 1))])
+def test_staged_shadow_matches_oracle_projection(conn, dims, regime):
+    """pcb_shadow on the fp32 state == oracle Pi_K of the same z (fp64 arithmetic)."""
+    from oracle import oracle as orc
+    from paracut_b200 import _native
+    from paracut_b200.graph import DIRECTIONS, direction_shape
+    rng = np.random.default_rng(hash((conn, dims, regime)) % 2 ** 31)
+    n = int(np.prod(dims))
+    shapes = [direction_shape(dims, d) for d in DIRECTIONS[conn]]
+    g = pc.GridEnergy(dims, conn, rng.normal(0, 3, n), _weights_regime(rng, shapes, regime))
+    S = _native.GridSolver(g, precision="f32")
+    z = rng.normal(0, 4, size=(S.r, n)) + rng.normal(0, 200, size=n)[None, :]
+    S.set_z(z)
+    z_used = S.get_z()
+    y, _ = S.shadow(want_y=True)
+    want = orc.project_K(orc.decompose(g), z_used)
+    scale = max(1.0, float(np.max(np.abs(want))))
+    assert np.max(np.abs(y - want)) <= 1e-9 * scale * 1e3
+
+
+@pytest.mark.parametrize("conn,dims", [("2D-4", (64, 70)), ("2D-8", (50, 61)),
+                                       ("3D-6", (12, 20, 33))])
+def test_staged_step_matches_oracle_iteration(conn, dims):
+    """a few fused fp32 iterations == the reference loop on the same start point."""
+    from oracle import oracle as orc
+    spec = {"2D-4": CONFIGS["cfg2_int"], "2D-8": CONFIGS["cfg3"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=11, dims=dims)
+    from paracut_b200 import _native
+    S = _native.GridSolver(g, precision="f32")
+    S.init_cold()
+    z0 = S.get_z()
+    norms = S.run(5)
+    z_gpu = S.get_z()
+    z_ref, _, norms_ref = orc.aar(g, 5, z=z0, threads=4)
+    assert _rel(z_gpu, z_ref) <= 1e-5
+    assert np.allclose(norms, norms_ref, rtol=1e-4)
