@@ -1003,7 +1003,7 @@ int shadow_fast(pcb_solver* h) {
     const Fam& F = h->fam[j];
     if (F.C == 0) continue;
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
-                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, nullptr};
+                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p};
     if (int rc = launch_role<pcb::fast::SHADOW>(h, a)) return rc;
   }
   return 0;
