@@ -23,14 +23,15 @@
 // only entries its cone tests read -- as (gate, slope) pairs, so the cone
 // tests are plain compares and a bend's prox value is the stored slope:
 // (y_bend - y_anchor)/(bk - i0) equals the reference's (sum + tube
-// offsets)/len.  Slopes use exact reciprocals of the small integer offsets
-// from a shared table.  Closing a segment is O(1): the lane writes
+// offsets)/len.  Slopes use a MUFU reciprocal of the small integer offset
+// refined by one fp64 Newton step.  Closing a segment is O(1): the lane writes
 // q = z_i0 - fill at the segment start and sets a start bit; per-node
 // outputs are produced by a lockstep retire pass over whole tiles
 // (p_new = (z_j - z_start) + q) and written back coalesced.  A lane whose
 // anchor falls behind the ring reads and writes those positions in global
 // memory; retirement is masked by each lane's emitted frontier.
 #pragma once
+#include <type_traits>
 
 namespace pcb {
 namespace fast {
@@ -39,7 +40,6 @@ constexpr int TP = 8;          // positions per tile
 constexpr int NT = 4;          // tiles in the ring
 constexpr int RL = TP * NT;    // ring length (positions)
 constexpr int WARPS = 4;       // warps per block
-constexpr int INV_N = 64;      // reciprocal table size
 static_assert(RL == 32, "swizzle and start masks assume a 32-position ring");
 static_assert(TP == 8, "mode-B lane mapping assumes 8-position tiles");
 
@@ -75,6 +75,28 @@ __device__ __forceinline__ void cp_wait(int pending) {
     case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
     default: asm volatile("cp.async.wait_group 3;\n" ::); break;
   }
+}
+
+// 1/d for a small positive integer d: MUFU approximation + one fp64 Newton step
+// (relative error ~2^-46, plenty for slope comparisons and segment values).
+__device__ __forceinline__ double rcp_small(int di, double dd) {
+  float r32;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r32) : "f"((float)di));
+  const double r = (double)r32;
+  return __fma_rn(r, __fma_rn(-dd, r, 1.0), r);
+}
+
+template <class Rt>
+__device__ __forceinline__ Rt rcp_r(int di);
+template <>
+__device__ __forceinline__ float rcp_r<float>(int di) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)di));
+  return r;
+}
+template <>
+__device__ __forceinline__ double rcp_r<double>(int di) {
+  return rcp_small(di, (double)di);
 }
 
 // ring index of (lane row l, position pos)
@@ -123,14 +145,11 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
 template <int ROLE, bool ROWLIKE>
 __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double inv_tab[INV_N];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const Fam F = A.F;
   const int64_t c0 = ((int64_t)blockIdx.x * WARPS + wib) * 32;
   double nrm = 0.0;
-  for (int t = threadIdx.x; t < INV_N; t += blockDim.x) inv_tab[t] = t ? 1.0 / (double)t : 0.0;
-  __syncthreads();
 
   unsigned char* base = smem_raw + (size_t)wib * ring_bytes_host<ROLE>();
   double* rz = reinterpret_cast<double*>(base);
@@ -147,11 +166,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   const int64_t my_base = valid ? fam_base(F, c) : 0;
   const int64_t C = F.C;
 
-  // ---- lane state: stackless taut string in the anchor frame
+  // ---- lane state: stackless taut string in the anchor frame.  The scan runs
+  // in R = fp32 for the in-place roles (values are taken relative to the
+  // anchor's z, so they stay O(|p| + local drift) and fp32 keeps ~1e-7 of
+  // them) and in fp64 for the shadow, whose output feeds the certificates.
+  using R = typename std::conditional<ROLE == SHADOW, double, float>::type;
   int i0 = 0, pe = m, k = 0, c0x = -1, f0x = -1;
-  double skr = 0.0;   // running sum minus the anchor value
-  double cs = 0.0;    // min slope anchor -> ceiling points
-  double fs = 0.0;    // max slope anchor -> floor points
+  double t = 0.0;          // z at the anchor: scan values are z - t
+  bool fresh = true;       // t is taken from the first gate after a (re)start
+  R skr = R(0);            // running sum of (z - t) minus the anchor value
+  R cs = R(0), Lc = R(0);  // min slope to the ceiling points; cs * (k - i0)
+  R fs = R(0), Lf = R(0);  // max slope to the floor points;   fs * (k - i0)
   bool done = !valid;
   unsigned smask = 0u;        // segment starts inside the ring (bit = slot)
   double zs = 0.0, qs = 0.0;  // retire carry: z at the current segment start, q there
@@ -292,6 +317,92 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     }
   };
 
+  // one round of scanning; LAG: some lane's anchor is below the ring
+  auto scan = [&](int lo_pos, int avail_hi, auto lag_tag) {
+    constexpr bool LAG = decltype(lag_tag)::value;
+    for (;;) {
+      const bool act = !done && k < avail_hi;
+      if (!__any_sync(0xffffffffu, act)) break;
+      if (act) {
+        const int kp = k;
+        const int ix = rix(lane, kp);
+        double zabs = rz[ix];
+        float af = ra[ix];
+        if (LAG && kp < lo_pos) {  // lagging lane below the ring
+          const int64_t fi = (int64_t)kp * C + c;
+          zabs = z_global(A, fi, fam_node(F, my_base, kp));
+          af = kp < m - 1 ? (float)a_global(A, fi) : 0.f;
+        }
+        k = kp + 1;
+        t = fresh ? zabs : t;
+        fresh = false;
+        skr += (R)(zabs - t);
+        const bool inner = k < m;
+        const R rk = inner ? (R)af : R(0);
+        pe = (inner && af == 0.f) ? k : pe;
+        const R inv = rcp_r<R>(k - i0);
+        Lc += cs;
+        Lf += fs;
+        // ceiling: keep the minimum slope from the anchor
+        const R u = skr + rk;
+        const bool cu = c0x < 0 || u <= Lc;
+        c0x = cu ? k : c0x;
+        cs = cu ? u * inv : cs;
+        Lc = cu ? u : Lc;
+        const bool b1 = f0x >= 0 && cs < fs;  // ceiling dips under the floor cone
+        // floor: keep the maximum slope (not pushed when b1 already bends)
+        const R l = skr - rk;
+        const bool fu = !b1 && (f0x < 0 || l >= Lf);
+        f0x = fu ? k : f0x;
+        fs = fu ? l * inv : fs;
+        Lf = fu ? l : Lf;
+        const bool b2 = !b1 && fs > cs;       // floor rises over the ceiling cone
+        const bool e = !b1 && !b2 && k == pe;  // piece end: S_pe is mandatory
+        const bool ec = e && c0x != pe && Lc < skr;
+        const bool ef = e && !ec && f0x != pe && Lf > skr;
+        const bool bend = b1 || b2 || e;
+        const bool tf = b1 || ef;  // touches the floor
+        const bool tc = b2 || ec;  // touches the ceiling
+        const int bk = tf ? f0x : (tc ? c0x : pe);
+        const R fill = tf ? fs : (tc ? cs : skr * inv);
+        // ---- close segment [i0, bk): its prox value is the string slope `fill` (+ t)
+        R ab = (R)ra[rix(lane, bk - 1)];
+        int s0 = i0;
+        R qv = -fill;  // q = z_i0 - fill, and z_i0 - t = 0
+        if (LAG && bend && i0 < lo_pos) {
+          const double fabs_ = (double)fill + t;
+          if (bk - 1 < lo_pos) ab = (R)a_global(A, (int64_t)(bk - 1) * C + c);
+          const int e2 = min(bk, lo_pos);
+          for (int j = i0; j < e2; ++j)
+            nrm += finish_global<ROLE>(A, (int64_t)j * C + c, fam_node(F, my_base, j), fabs_);
+          s0 = e2;
+          if (s0 < bk) qv = (R)((rz[rix(lane, s0)] - t) - (double)fill);
+        }
+        const bool mark = bend && (!LAG || s0 < bk);
+        const int ixs = rix(lane, s0);
+        if (mark) {
+          if (ROLE == SHADOW) rf[ixs] = (double)qv;
+          else ra[ixs] = (float)qv;
+        }
+        smask |= mark ? (1u << (s0 & (RL - 1))) : 0u;
+        const bool piece_end = bk == pe;
+        const R nskr = piece_end ? R(0) : (tf ? ab : (tc ? -ab : R(0)));
+        i0 = bend ? bk : i0;
+        k = bend ? bk : k;
+        fresh = bend;
+        skr = bend ? nskr : skr;
+        pe = (bend && piece_end) ? m : pe;
+        done = bend && bk >= m;
+        c0x = bend ? -1 : c0x;
+        f0x = bend ? -1 : f0x;
+        cs = bend ? R(0) : cs;
+        fs = bend ? R(0) : fs;
+        Lc = bend ? R(0) : Lc;
+        Lf = bend ? R(0) : Lf;
+      }
+    }
+  };
+
   if (warp_live) {
     while (t_ld < ntiles && t_ld < NT) issue(t_ld++);
     cp_wait(t_ld - 1);
@@ -302,91 +413,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       const int lo_pos = t_lo * TP;
       const int avail_hi = min(t_rdy * TP, m);
       if (pre_tile != t_lo) prefetch(t_lo);
-      // ---------------- scan until every lane needs data beyond avail_hi
-      while (!done && k < avail_hi) {
-        const int kp = k;
-        double zv, av = 0.0;
-        if (kp >= lo_pos) {
-          const int ix = rix(lane, kp);
-          zv = rz[ix];
-          av = ra[ix];
-        } else {
-          const int64_t fi = (int64_t)kp * C + c;
-          zv = z_global(A, fi, fam_node(F, my_base, kp));
-          if (kp < m - 1) av = a_global(A, fi);
-        }
-        k = kp + 1;
-        skr += zv;
-        const int dki = k - i0;
-        const double inv = dki < INV_N ? inv_tab[dki] : 1.0 / (double)dki;
-        double rk = 0.0;
-        if (k < m) {
-          rk = av;
-          if (rk == 0.0) pe = k;
-        }
-        const double su = (skr + rk) * inv;
-        if (c0x < 0 || su <= cs) {
-          c0x = k;
-          cs = su;
-        }
-        int bk = -1, bt = 0;
-        double fill = 0.0;
-        if (f0x >= 0 && cs < fs) {
-          bk = f0x; fill = fs; bt = -1;
-        } else {
-          const double sl = (skr - rk) * inv;
-          if (f0x < 0 || sl >= fs) {
-            f0x = k;
-            fs = sl;
-          }
-          if (fs > cs) {
-            bk = c0x; fill = cs; bt = 1;
-          } else if (k == pe) {
-            const double sa = skr * inv;
-            if (c0x != pe && cs < sa) {
-              bk = c0x; fill = cs; bt = 1;
-            } else if (f0x != pe && fs > sa) {
-              bk = f0x; fill = fs; bt = -1;
-            } else {
-              bk = pe; fill = sa; bt = 0;
-            }
-          }
-        }
-        if (bk >= 0) {
-          // close segment [i0, bk): its prox value is the string slope `fill`
-          double nskr = 0.0;
-          if (bt != 0) {
-            const int pa = bk - 1;
-            const double ab = pa >= lo_pos ? (double)ra[rix(lane, pa)]
-                                           : a_global(A, (int64_t)pa * C + c);
-            nskr = -(double)bt * ab;
-          }
-          int s0 = i0;
-          if (s0 < lo_pos) {  // lagging lane: the part below the ring goes straight to memory
-            const int e = min(bk, lo_pos);
-            for (int j = s0; j < e; ++j)
-              nrm += finish_global<ROLE>(A, (int64_t)j * C + c, fam_node(F, my_base, j), fill);
-            s0 = e;
-          }
-          if (s0 < bk) {
-            const int ix = rix(lane, s0);
-            const double qv = rz[ix] - fill;
-            if (ROLE == SHADOW) rf[ix] = qv;
-            else ra[ix] = (float)qv;
-            smask |= 1u << (s0 & (RL - 1));
-          }
-          i0 = bk;
-          if (i0 == pe) {
-            pe = m;
-            skr = 0.0;
-            done = i0 >= m;
-          } else {
-            skr = nskr;
-          }
-          k = i0;
-          c0x = f0x = -1;
-        }
-      }
+      // ---------------- scan until every lane needs data beyond avail_hi.
+      // One gate per trip.  Warps with no lagging lane (the normal case) run
+      // a variant without any below-the-ring checks, with the segment close
+      // fully predicated so the warp stays converged through bends.
+      if (__any_sync(0xffffffffu, !done && i0 < lo_pos))
+        scan(lo_pos, avail_hi, std::true_type());
+      else
+        scan(lo_pos, avail_hi, std::false_type());
       __syncwarp();
       if (__all_sync(0xffffffffu, done)) {
         cp_wait(0);
