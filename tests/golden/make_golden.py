@@ -80,10 +80,15 @@ def save(name, **arrays):
     print("wrote", path, os.path.getsize(path), "bytes")
 
 
+_PC = None
+
+
 def grid_arrays(g, prefix=""):
     d = {prefix + "dims": np.array(g.dims, dtype=np.int64),
          prefix + "conn": np.array(g.connectivity),
          prefix + "w": g.w}
+    if _PC is not None:
+        d[prefix + "fingerprint"] = np.array(_PC.instance_fingerprint(g))
     for k, a in enumerate(g.dir_weights):
         d[prefix + "dw%d" % k] = a
     return d
@@ -109,7 +114,9 @@ def fixed_iter(pc, g, ks):
 
 
 def main():
+    global _PC
     pc = import_reference()
+    _PC = pc
     sys.path.insert(0, REPO)
     from paracut_b200.instances import CONFIGS, make_instance
 
