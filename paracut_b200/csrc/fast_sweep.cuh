@@ -55,6 +55,12 @@ struct Args {
   double* y;        // SHADOW output (natural)
   double inv_r, rd;
   double* parts;    // per-block monitor partials
+  // intra-chain split (nullptr: whole chains).  Unit (chain c, block b) runs
+  // the string from the merge point of block b (merge[b*C + c]; block 0 starts
+  // at the chain start) up to the next block's merge point.  Code:
+  // pos * 4 + (touch + 1), touch -1 floor / +1 ceiling / 0 piece start; -1 none.
+  const int* merge;
+  int nb;
 };
 
 __device__ __forceinline__ void cp4(void* dst, const void* src, bool pred) {
@@ -162,22 +168,53 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   const bool valid = lane < nvalid;
   const int64_t c = c0 + lane;
   const int m = F.m;
-  const int ntiles = (m + TP - 1) / TP;
   const int64_t my_base = valid ? fam_base(F, c) : 0;
   const int64_t C = F.C;
+
+  // this unit's range [start, stop) of the chain and the tube touches there;
+  // the string is forced through the next unit's merge point at gate `stop`
+  // (a true point of the string), so a unit never reads past its range and
+  // units of one chain never race on the in-place state
+  int start = 0, stop = m, stouch = 0, etouch = 0;
+  bool has = valid;
+  if (A.merge != nullptr && valid) {
+    const int b = blockIdx.y;
+    if (b > 0) {
+      const int e = A.merge[(int64_t)b * C + c];
+      has = e >= 0;
+      start = e >> 2;
+      stouch = (e & 3) - 1;
+    }
+    for (int b2 = b + 1; b2 < A.nb; ++b2) {
+      const int e = A.merge[(int64_t)b2 * C + c];
+      if (e >= 0) {
+        stop = e >> 2;
+        etouch = (e & 3) - 1;
+        break;
+      }
+    }
+    if (!has || start >= stop) {
+      has = false;
+      start = stop = 0;
+    }
+  }
+  const int rlo = __reduce_min_sync(0xffffffffu, has ? start : 0x7fffffff);
+  const int rhi = __reduce_max_sync(0xffffffffu, has ? stop : 0);
+  const int t_first = rlo == 0x7fffffff ? 0 : rlo / TP;
+  const int ntiles = (rhi + TP - 1) / TP;
 
   // ---- lane state: stackless taut string in the anchor frame.  The scan runs
   // in R = fp32 for the in-place roles (values are taken relative to the
   // anchor's z, so they stay O(|p| + local drift) and fp32 keeps ~1e-7 of
   // them) and in fp64 for the shadow, whose output feeds the certificates.
   using R = typename std::conditional<ROLE == SHADOW, double, float>::type;
-  int i0 = 0, pe = m, k = 0, c0x = -1, f0x = -1;
+  int i0 = start, pe = m, k = start, c0x = -1, f0x = -1;
   double t = 0.0;          // z at the anchor: scan values are z - t
   bool fresh = true;       // t is taken from the first gate after a (re)start
   R skr = R(0);            // running sum of (z - t) minus the anchor value
   R cs = R(0), Lc = R(0);  // min slope to the ceiling points; cs * (k - i0)
   R fs = R(0), Lf = R(0);  // max slope to the floor points;   fs * (k - i0)
-  bool done = !valid;
+  bool done = !has;
   unsigned smask = 0u;        // segment starts inside the ring (bit = slot)
   double zs = 0.0, qs = 0.0;  // retire carry: z at the current segment start, q there
 
@@ -185,7 +222,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   float gpre[TP], xpre[TP];
   int pre_tile = -1;
 
-  int t_lo = 0, t_ld = 0, t_rdy = 0;
+  int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
+  if (has && start > 0 && stouch != 0)  // anchored on a tube touch: skr = -touch * a(start-1)
+    skr = (R)(-(double)stouch * (double)A.wf[(int64_t)(start - 1) * C + c]);
+  // end value offset at `stop`: the string ends at S_stop + touch * a(stop-1)
+  const R eoff = (has && stop < m && etouch != 0)
+                     ? (R)((double)etouch * (double)A.wf[(int64_t)(stop - 1) * C + c]) : R(0);
 
   auto issue = [&](int T) {
     const int k0 = T * TP;
@@ -258,7 +300,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
-      if (valid && pos < m && pos < i0) {
+      if (has && pos >= start && pos < stop && pos < i0) {
         const int slot = pos & (RL - 1);
         const int ix = rix(lane, pos);
         const double zj = rz[ix];
@@ -304,8 +346,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
         const int i0_i = __shfl_sync(0xffffffffu, i0, i);
+        const int st_i = __shfl_sync(0xffffffffu, start, i);
+        const int sp_i = __shfl_sync(0xffffffffu, stop, i);
+        const bool has_i = __shfl_sync(0xffffffffu, has, i);
         const int64_t bi = __shfl_sync(0xffffffffu, my_base, i);
-        if (i < nvalid && pos < m && pos < i0_i) {
+        if (has_i && pos >= st_i && pos < sp_i && pos < i0_i) {
           const int ix = rix(i, pos);
           const int64_t nd = fam_node(F, bi, pos);
           if (ROLE == SHADOW) A.y[nd] = rz[ix];
@@ -337,34 +382,36 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         t = fresh ? zabs : t;
         fresh = false;
         skr += (R)(zabs - t);
-        const bool inner = k < m;
+        const bool at_stop = k == stop;  // forced end point (merge point or chain end)
+        const bool inner = k < m && !at_stop;
         const R rk = inner ? (R)af : R(0);
-        pe = (inner && af == 0.f) ? k : pe;
+        pe = ((inner && af == 0.f) || at_stop) ? k : pe;
         const R inv = rcp_r<R>(k - i0);
         Lc += cs;
         Lf += fs;
+        const R sE = at_stop ? skr + eoff : skr;  // string value required at an end gate
         // ceiling: keep the minimum slope from the anchor
-        const R u = skr + rk;
+        const R u = sE + rk;
         const bool cu = c0x < 0 || u <= Lc;
         c0x = cu ? k : c0x;
         cs = cu ? u * inv : cs;
         Lc = cu ? u : Lc;
         const bool b1 = f0x >= 0 && cs < fs;  // ceiling dips under the floor cone
         // floor: keep the maximum slope (not pushed when b1 already bends)
-        const R l = skr - rk;
+        const R l = sE - rk;
         const bool fu = !b1 && (f0x < 0 || l >= Lf);
         f0x = fu ? k : f0x;
         fs = fu ? l * inv : fs;
         Lf = fu ? l : Lf;
         const bool b2 = !b1 && fs > cs;       // floor rises over the ceiling cone
         const bool e = !b1 && !b2 && k == pe;  // piece end: S_pe is mandatory
-        const bool ec = e && c0x != pe && Lc < skr;
-        const bool ef = e && !ec && f0x != pe && Lf > skr;
+        const bool ec = e && c0x != pe && Lc < sE;
+        const bool ef = e && !ec && f0x != pe && Lf > sE;
         const bool bend = b1 || b2 || e;
         const bool tf = b1 || ef;  // touches the floor
         const bool tc = b2 || ec;  // touches the ceiling
         const int bk = tf ? f0x : (tc ? c0x : pe);
-        const R fill = tf ? fs : (tc ? cs : skr * inv);
+        const R fill = tf ? fs : (tc ? cs : sE * inv);
         // ---- close segment [i0, bk): its prox value is the string slope `fill` (+ t)
         R ab = (R)ra[rix(lane, bk - 1)];
         int s0 = i0;
@@ -372,13 +419,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         if (LAG && bend && i0 < lo_pos) {
           const double fabs_ = (double)fill + t;
           if (bk - 1 < lo_pos) ab = (R)a_global(A, (int64_t)(bk - 1) * C + c);
-          const int e2 = min(bk, lo_pos);
+          const int e2 = min(min(bk, lo_pos), stop);
           for (int j = i0; j < e2; ++j)
             nrm += finish_global<ROLE>(A, (int64_t)j * C + c, fam_node(F, my_base, j), fabs_);
           s0 = e2;
           if (s0 < bk) qv = (R)((rz[rix(lane, s0)] - t) - (double)fill);
         }
-        const bool mark = bend && (!LAG || s0 < bk);
+        const bool mark = bend && s0 < stop && (!LAG || s0 < bk);
         const int ixs = rix(lane, s0);
         if (mark) {
           if (ROLE == SHADOW) rf[ixs] = (double)qv;
@@ -392,7 +439,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         fresh = bend;
         skr = bend ? nskr : skr;
         pe = (bend && piece_end) ? m : pe;
-        done = bend && bk >= m;
+        done = bend && bk >= stop;
         c0x = bend ? -1 : c0x;
         f0x = bend ? -1 : f0x;
         cs = bend ? R(0) : cs;
@@ -403,12 +450,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     }
   };
 
-  if (warp_live) {
-    while (t_ld < ntiles && t_ld < NT) issue(t_ld++);
-    cp_wait(t_ld - 1);
+  if (warp_live && rhi > 0) {
+    while (t_ld < ntiles && t_ld - t_first < NT) issue(t_ld++);
+    cp_wait(t_ld - t_first - 1);
     __syncwarp();
-    to_z(0);
-    t_rdy = 1;
+    to_z(t_first);
+    t_rdy = t_first + 1;
     for (;;) {
       const int lo_pos = t_lo * TP;
       const int avail_hi = min(t_rdy * TP, m);
@@ -450,9 +497,138 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     if (threadIdx.x == 0) {
       double t = 0.0;
       for (int w = 0; w < WARPS; ++w) t += sh[w];
-      A.parts[blockIdx.x] = t;
+      A.parts[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = t;
     }
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Intra-chain split: merge points.  For block b >= 1 of chain c the true
+// string crosses gate g = b * lb somewhere inside the tube [S_g - a, S_g + a].
+// The taut strings anchored at the floor point and at the ceiling point of
+// that gate bracket it (taut strings to a common end point never cross), so
+// at their first common tube touch all three coincide and stay equal.  Each
+// thread scans both speculative strings (fp64 stackless scan, data from
+// global memory) bend by bend until they share a bend point, or gives up
+// after `window` positions (merge = -1: the previous unit continues).
+struct Spec {
+  int i0, pe, k, c0x, f0x;
+  double t, skr, cs, fs, Lc, Lf;
+  bool fresh;
+};
+
+template <class ZA>
+__device__ __forceinline__ void spec_next_bend(Spec& S, int m, const ZA& za, int* bk_out,
+                                               int* bt_out) {
+  for (;;) {
+    const int kp = S.k;
+    double zabs, av;
+    za(kp, &zabs, &av);
+    S.k = kp + 1;
+    if (S.fresh) {
+      S.t = zabs;
+      S.fresh = false;
+    }
+    S.skr += zabs - S.t;
+    const bool inner = S.k < m;
+    const double rk = inner ? av : 0.0;
+    if (inner && av == 0.0) S.pe = S.k;
+    const double inv = 1.0 / (double)(S.k - S.i0);
+    S.Lc += S.cs;
+    S.Lf += S.fs;
+    const double u = S.skr + rk;
+    if (S.c0x < 0 || u <= S.Lc) {
+      S.c0x = S.k;
+      S.cs = u * inv;
+      S.Lc = u;
+    }
+    int bk = -1, bt = 0;
+    double fill = 0.0;
+    if (S.f0x >= 0 && S.cs < S.fs) {
+      bk = S.f0x; bt = -1; fill = S.fs;
+    } else {
+      const double l = S.skr - rk;
+      if (S.f0x < 0 || l >= S.Lf) {
+        S.f0x = S.k;
+        S.fs = l * inv;
+        S.Lf = l;
+      }
+      if (S.fs > S.cs) {
+        bk = S.c0x; bt = 1; fill = S.cs;
+      } else if (S.k == S.pe) {
+        if (S.c0x != S.pe && S.Lc < S.skr) {
+          bk = S.c0x; bt = 1; fill = S.cs;
+        } else if (S.f0x != S.pe && S.Lf > S.skr) {
+          bk = S.f0x; bt = -1; fill = S.fs;
+        } else {
+          bk = S.pe; bt = 0; fill = S.skr * inv;
+        }
+      }
+    }
+    if (bk >= 0) {
+      (void)fill;
+      double ab = 0.0;
+      if (bt != 0) {
+        double dz;
+        za(bk - 1, &dz, &ab);
+      }
+      const bool piece_end = bk == S.pe;
+      S.i0 = S.k = bk;
+      S.fresh = true;
+      S.skr = piece_end ? 0.0 : -(double)bt * ab;
+      if (piece_end) S.pe = m;
+      S.c0x = S.f0x = -1;
+      S.cs = S.fs = S.Lc = S.Lf = 0.0;
+      *bk_out = bk;
+      *bt_out = piece_end ? 0 : bt;
+      return;
+    }
+  }
+}
+
+__global__ void k_merge(Fam F, const float* p, const float* wf, const double* cdr, int lb, int nb,
+                        int window, int* merge) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int b = blockIdx.y + 1;
+  if (c >= F.C || b >= nb) return;
+  const int64_t C = F.C;
+  const int m = F.m;
+  const int64_t base = fam_base(F, c);
+  auto za = [&](int pos, double* z, double* a) {
+    const int64_t fi = (int64_t)pos * C + c;
+    *z = (double)__ldg(p + fi) + __ldg(cdr + fam_node(F, base, pos));
+    *a = pos < m - 1 ? (double)__ldg(wf + fi) : 0.0;
+  };
+  const int g = b * lb;
+  int out = -1;
+  if (g < m) {
+    const double ag = (double)__ldg(wf + (int64_t)(g - 1) * C + c);
+    if (ag == 0.0) {
+      out = g * 4 + 1;  // zero-weight gate: a piece starts here for every string
+    } else {
+      Spec Fs{g, m, g, -1, -1, 0.0, ag, 0.0, 0.0, 0.0, 0.0, true};
+      Spec Us{g, m, g, -1, -1, 0.0, -ag, 0.0, 0.0, 0.0, 0.0, true};
+      int pf, tf, pu, tu;
+      spec_next_bend(Fs, m, za, &pf, &tf);
+      spec_next_bend(Us, m, za, &pu, &tu);
+      const int lim = min(m, g + window);
+      while (pf < lim || pu < lim) {
+        if (pf == pu && tf == tu) {
+          if (pf < m) out = pf * 4 + (tf + 1);
+          break;
+        }
+        if (pf <= pu) {
+          if (pf >= lim) break;
+          spec_next_bend(Fs, m, za, &pf, &tf);
+        } else {
+          if (pu >= lim) break;
+          spec_next_bend(Us, m, za, &pu, &tu);
+        }
+      }
+    }
+  }
+  merge[(int64_t)b * C + c] = out;
 }
 
 }  // namespace fast

@@ -24,6 +24,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -719,6 +720,9 @@ struct pcb_solver {
   DBuf<double> sp_cy, sp_fy;
   DBuf<uint8_t> packed;
   int64_t spill_per = 0;  // spill entries per thread
+  int nbk[MAXR]{};        // fp32 path: blocks per chain (intra-chain split), 1 = whole chains
+  int lbk[MAXR]{};        // block length (positions)
+  DBuf<int> merge;        // merge points, max_j nbk[j] * C_j
   // profiling: event pairs around family launches
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -960,7 +964,7 @@ int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
   CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   const int per = pcb::fast::WARPS * 32;
-  const int g = (int)((a.F.C + per - 1) / per);
+  const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
   pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a);
   LAUNCH_CHECK(h);
   return 0;
@@ -969,6 +973,26 @@ int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
 template <int ROLE>
 int launch_role(pcb_solver* h, const pcb::fast::Args& a) {
   return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a) : launch_sweep<ROLE, false>(h, a);
+}
+
+// merge points of family j for the current state (before its sweep)
+int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) {
+  a.merge = nullptr;
+  a.nb = 1;
+  if (h->nbk[j] <= 1) return 0;
+  const Fam& F = h->fam[j];
+  const dim3 g((unsigned)((F.C + 127) / 128), (unsigned)(h->nbk[j] - 1));
+  pcb::fast::k_merge<<<g, 128, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+                                                 4 * h->lbk[j], h->merge.p);
+  LAUNCH_CHECK(h);
+  a.merge = h->merge.p;
+  a.nb = h->nbk[j];
+  return 0;
+}
+
+int fam_units(const pcb_solver* h, int j) {
+  const int per = pcb::fast::WARPS * 32;
+  return (int)((h->fam[j].C + per - 1) / per) * (h->nbk[j] > 1 ? h->nbk[j] : 1);
 }
 
 // one fused fp32 iteration; partials of every family land in parts[], reduced in order
@@ -981,17 +1005,18 @@ int step_fast(pcb_solver* h, double* norm_slot) {
     if (F.C == 0) continue;  // only zig-zags can be empty, never first/last
     const int role = (q == 0) ? pcb::fast::FIRST : (q == h->r - 1 ? pcb::fast::LAST
                                                                    : pcb::fast::MID);
-    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
-                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off};
+                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1};
     prof_begin(h, j);
-    int rc;
-    if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a);
-    else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a);
-    else rc = launch_sweep<pcb::fast::LAST, false>(h, a);
+    int rc = launch_merge(h, j, a);
+    if (!rc) {
+      if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a);
+      else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a);
+      else rc = launch_sweep<pcb::fast::LAST, false>(h, a);
+    }
     prof_end(h);
     if (rc) return rc;
-    off += g;
+    off += fam_units(h, j);
   }
   k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot, 1);
   LAUNCH_CHECK(h);
@@ -1003,15 +1028,44 @@ int shadow_fast(pcb_solver* h) {
     const Fam& F = h->fam[j];
     if (F.C == 0) continue;
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
-                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p};
+                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p, nullptr, 1};
+    if (int rc = launch_merge(h, j, a)) return rc;
     if (int rc = launch_role<pcb::fast::SHADOW>(h, a)) return rc;
   }
   return 0;
 }
 
+// Blocks per chain for the fp32 sweep: enough (chain group x block) units to
+// fill the machine ~4 times over, blocks of at least 32 positions.
+int choose_split(pcb_solver* h) {
+  int64_t need = 0;
+  const char* env = getenv("PCB_SPLIT_TARGET");  // tuning knob (warps)
+  const int64_t target = env ? atoll(env) : 148 * 12 * 4;
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    const int64_t warps = (F.C + 31) / 32;
+    int nb = 1;
+    if (F.C > 0 && warps < target && F.m >= 64) {
+      nb = (int)((target + warps - 1) / warps);
+      const int maxb = F.m / 32;
+      if (nb > maxb) nb = maxb;
+      if (nb < 1) nb = 1;
+    }
+    int lb = (F.m + nb - 1) / nb;
+    lb = (lb + 7) & ~7;
+    nb = (F.m + lb - 1) / lb;
+    h->nbk[j] = nb;
+    h->lbk[j] = lb;
+    if (nb > 1 && (int64_t)nb * F.C > need) need = (int64_t)nb * F.C;
+  }
+  if (need > 0)
+    if (int e = h->merge.alloc(need)) return e;
+  return 0;
+}
+
 int parts_needed(const pcb_solver* h) {
   int64_t fam_blocks = 0;
-  for (int j = 0; j < h->r; ++j) fam_blocks += (h->fam[j].C + FAM_BLOCK - 1) / FAM_BLOCK;
+  for (int j = 0; j < h->r; ++j) fam_blocks += fam_units(h, j) + (h->fam[j].C + FAM_BLOCK - 1) / FAM_BLOCK;
   int64_t need = fam_blocks;
   const int64_t node = (int64_t)NODE_GRID * (MAXT + 3);
   if (node > need) need = node;
@@ -1092,6 +1146,7 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
     if ((rc = h->X32.alloc(n))) return bail(rc);
     if ((rc = h->G32.alloc(n))) return bail(rc);
     if ((rc = ensure_wf32(h))) return bail(rc);
+    if ((rc = choose_split(h))) return bail(rc);
   }
   if ((rc = ensure_spill(h))) return bail(rc);
   if ((rc = h->bits.alloc(n))) return bail(rc);

@@ -117,3 +117,30 @@ def test_staged_step_matches_oracle_iteration(conn, dims):
     z_ref, _, norms_ref = orc.aar(g, 5, z=z0, threads=4)
     assert _rel(z_gpu, z_ref) <= 1e-5
     assert np.allclose(norms, norms_ref, rtol=1e-4)
+
+
+@pytest.mark.parametrize("target", ["1", "100000"])
+@pytest.mark.parametrize("conn,dims", [("2D-4", (64, 520)), ("2D-8", (40, 333)),
+                                       ("3D-6", (7, 9, 300))])
+def test_intra_chain_split_matches_oracle(monkeypatch, target, conn, dims):
+    """Chains cut into blocks joined at speculative merge points give the same
+    prox (shadow to ~1e-9) and iterates (1e-4) as whole chains."""
+    from oracle import oracle as orc
+    from paracut_b200 import _native
+    monkeypatch.setenv("PCB_SPLIT_TARGET", target)
+    spec = {"2D-4": CONFIGS["cfg2_int"], "2D-8": CONFIGS["cfg3"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=3, dims=dims)
+    S = _native.GridSolver(g, precision="f32")
+    S.init_cold()
+    S.run(7)
+    z = S.get_z()
+    y, _ = S.shadow(want_y=True)
+    want = orc.project_K(orc.decompose(g), z)
+    assert np.max(np.abs(y - want)) <= 1e-9 * max(1.0, float(np.max(np.abs(want)))) * 1e3
+    k = 60
+    z_ref, y_ref, _ = orc.aar(g, k, threads=4)
+    res = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=k, check_every=k + 1, precision="f32"))
+    x_ref = g.w - y_ref.sum(axis=0)
+    x = g.w - res.dual_state.y.sum(axis=0)
+    assert _rel(x, x_ref) <= 1e-4
