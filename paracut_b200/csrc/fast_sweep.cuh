@@ -365,14 +365,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   // one round of scanning; LAG: some lane's anchor is below the ring
   auto scan = [&](int lo_pos, int avail_hi, auto lag_tag) {
     constexpr bool LAG = decltype(lag_tag)::value;
+    // software-pipelined ring reads: the next gate's z and a are loaded at the
+    // end of the previous trip (slots >= k are never written by the scan)
+    double zn = rz[rix(lane, k)];
+    float an = ra[rix(lane, k)];
     for (;;) {
       const bool act = !done && k < avail_hi;
       if (!__any_sync(0xffffffffu, act)) break;
       if (act) {
         const int kp = k;
-        const int ix = rix(lane, kp);
-        double zabs = rz[ix];
-        float af = ra[ix];
+        double zabs = zn;
+        float af = an;
         if (LAG && kp < lo_pos) {  // lagging lane below the ring
           const int64_t fi = (int64_t)kp * C + c;
           zabs = z_global(A, fi, fam_node(F, my_base, kp));
@@ -446,6 +449,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         fs = bend ? R(0) : fs;
         Lc = bend ? R(0) : Lc;
         Lf = bend ? R(0) : Lf;
+        const int ixn = rix(lane, k);
+        zn = rz[ixn];
+        an = ra[ixn];
       }
     }
   };
@@ -534,7 +540,7 @@ __device__ __forceinline__ void spec_next_bend(Spec& S, int m, const ZA& za, int
     const bool inner = S.k < m;
     const double rk = inner ? av : 0.0;
     if (inner && av == 0.0) S.pe = S.k;
-    const double inv = 1.0 / (double)(S.k - S.i0);
+    const double inv = rcp_r<double>(S.k - S.i0);
     S.Lc += S.cs;
     S.Lf += S.fs;
     const double u = S.skr + rk;
@@ -587,44 +593,99 @@ __device__ __forceinline__ void spec_next_bend(Spec& S, int m, const ZA& za, int
   }
 }
 
-__global__ void k_merge(Fam F, const float* p, const float* wf, const double* cdr, int lb, int nb,
-                        int window, int* merge) {
-  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// One warp = 32 chains at block b.  The first MW positions from the block
+// gate are staged in shared memory with coalesced cp.async (mode A / mode B
+// like the sweep); merges almost always happen inside that window, positions
+// beyond it are read from global memory.
+constexpr int MW = 16;
+__device__ __forceinline__ int mix(int l, int q) { return l * MW + (q ^ (l & (MW - 1))); }
+
+template <bool ROWLIKE>
+__global__ void __launch_bounds__(WARPS * 32) k_merge(Fam F, const float* p, const float* wf,
+                                                      const double* cdr, int lb, int nb, int window,
+                                                      int* merge) {
+  __shared__ double sz[WARPS][32 * MW];
+  __shared__ float sa[WARPS][32 * MW];
+  __shared__ float sp[WARPS][32 * MW];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t c0 = ((int64_t)blockIdx.x * WARPS + wib) * 32;
   const int b = blockIdx.y + 1;
-  if (c >= F.C || b >= nb) return;
   const int64_t C = F.C;
   const int m = F.m;
-  const int64_t base = fam_base(F, c);
-  auto za = [&](int pos, double* z, double* a) {
-    const int64_t fi = (int64_t)pos * C + c;
-    *z = (double)__ldg(p + fi) + __ldg(cdr + fam_node(F, base, pos));
-    *a = pos < m - 1 ? (double)__ldg(wf + fi) : 0.0;
-  };
   const int g = b * lb;
-  int out = -1;
-  if (g < m) {
-    const double ag = (double)__ldg(wf + (int64_t)(g - 1) * C + c);
-    if (ag == 0.0) {
-      out = g * 4 + 1;  // zero-weight gate: a piece starts here for every string
+  if (c0 >= C || b >= nb || g >= m) return;  // warp-uniform
+  const int nvalid = (int)min((int64_t)32, C - c0);
+  const bool valid = lane < nvalid;
+  const int64_t c = c0 + lane;
+  const int64_t base = valid ? fam_base(F, c) : 0;
+  double* z_s = sz[wib];
+  float* a_s = sa[wib];
+  float* p_s = sp[wib];
+  // ---- stage positions [g, g + MW)
+#pragma unroll 4
+  for (int q = 0; q < MW; ++q) {
+    const int pos = g + q;
+    const bool pr = valid && pos < m;
+    const int64_t fi = pr ? (int64_t)pos * C + c : 0;
+    cp4(&p_s[mix(lane, q)], p + fi, pr);
+    cp4(&a_s[mix(lane, q)], wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
+    if (!ROWLIKE) cp8(&z_s[mix(lane, q)], cdr + (pr ? fam_node(F, base, pos) : 0), pr);
+  }
+  if (ROWLIKE) {
+#pragma unroll 4
+    for (int ib = 0; ib < 32; ib += 32 / MW) {
+      const int i = ib + lane / MW;
+      const int q = lane % MW;
+      const int64_t bi = __shfl_sync(0xffffffffu, base, i);
+      const int pos = g + q;
+      const bool pr = i < nvalid && pos < m;
+      cp8(&z_s[mix(i, q)], cdr + (pr ? fam_node(F, bi, pos) : 0), pr);
+    }
+  }
+  cp_commit();
+  cp_wait(0);
+  __syncwarp();
+#pragma unroll 4
+  for (int q = 0; q < MW; ++q) {
+    const int ix = mix(lane, q);
+    z_s[ix] = (double)p_s[ix] + z_s[ix];
+  }
+  __syncwarp();
+  if (!valid) return;
+  auto za = [&](int pos, double* z, double* a) {
+    const int q = pos - g;
+    if (q >= 0 && q < MW) {
+      const int ix = mix(lane, q);
+      *z = z_s[ix];
+      *a = (double)a_s[ix];
     } else {
-      Spec Fs{g, m, g, -1, -1, 0.0, ag, 0.0, 0.0, 0.0, 0.0, true};
-      Spec Us{g, m, g, -1, -1, 0.0, -ag, 0.0, 0.0, 0.0, 0.0, true};
-      int pf, tf, pu, tu;
-      spec_next_bend(Fs, m, za, &pf, &tf);
-      spec_next_bend(Us, m, za, &pu, &tu);
-      const int lim = min(m, g + window);
-      while (pf < lim || pu < lim) {
-        if (pf == pu && tf == tu) {
-          if (pf < m) out = pf * 4 + (tf + 1);
-          break;
-        }
-        if (pf <= pu) {
-          if (pf >= lim) break;
-          spec_next_bend(Fs, m, za, &pf, &tf);
-        } else {
-          if (pu >= lim) break;
-          spec_next_bend(Us, m, za, &pu, &tu);
-        }
+      const int64_t fi = (int64_t)pos * C + c;
+      *z = (double)__ldg(p + fi) + __ldg(cdr + fam_node(F, base, pos));
+      *a = pos < m - 1 ? (double)__ldg(wf + fi) : 0.0;
+    }
+  };
+  int out = -1;
+  const double ag = (double)__ldg(wf + (int64_t)(g - 1) * C + c);
+  if (ag == 0.0) {
+    out = g * 4 + 1;  // zero-weight gate: a piece starts here for every string
+  } else {
+    Spec Fs{g, m, g, -1, -1, 0.0, ag, 0.0, 0.0, 0.0, 0.0, true};
+    Spec Us{g, m, g, -1, -1, 0.0, -ag, 0.0, 0.0, 0.0, 0.0, true};
+    int pf, tf, pu, tu;
+    spec_next_bend(Fs, m, za, &pf, &tf);
+    spec_next_bend(Us, m, za, &pu, &tu);
+    const int lim = min(m, g + window);
+    while (pf < lim || pu < lim) {
+      if (pf == pu && tf == tu) {
+        if (pf < m) out = pf * 4 + (tf + 1);
+        break;
+      }
+      if (pf <= pu) {
+        if (pf >= lim) break;
+        spec_next_bend(Fs, m, za, &pf, &tf);
+      } else {
+        if (pu >= lim) break;
+        spec_next_bend(Us, m, za, &pu, &tu);
       }
     }
   }

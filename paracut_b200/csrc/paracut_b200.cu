@@ -981,9 +981,14 @@ int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) {
   a.nb = 1;
   if (h->nbk[j] <= 1) return 0;
   const Fam& F = h->fam[j];
-  const dim3 g((unsigned)((F.C + 127) / 128), (unsigned)(h->nbk[j] - 1));
-  pcb::fast::k_merge<<<g, 128, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
-                                                 4 * h->lbk[j], h->merge.p);
+  const int per = pcb::fast::WARPS * 32;
+  const dim3 g((unsigned)((F.C + per - 1) / per), (unsigned)(h->nbk[j] - 1));
+  if (fam_rowlike(F.kind))
+    pcb::fast::k_merge<true><<<g, per, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+                                                       4 * h->lbk[j], h->merge.p);
+  else
+    pcb::fast::k_merge<false><<<g, per, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+                                                        4 * h->lbk[j], h->merge.p);
   LAUNCH_CHECK(h);
   a.merge = h->merge.p;
   a.nb = h->nbk[j];
@@ -1040,7 +1045,7 @@ int shadow_fast(pcb_solver* h) {
 int choose_split(pcb_solver* h) {
   int64_t need = 0;
   const char* env = getenv("PCB_SPLIT_TARGET");  // tuning knob (warps)
-  const int64_t target = env ? atoll(env) : 148 * 12 * 4;
+  const int64_t target = env ? atoll(env) : 4096;
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
     const int64_t warps = (F.C + 31) / 32;
