@@ -17,10 +17,12 @@ events around each launch inside the timed region.  ``cpu_baseline`` is the
 oracle's C restatement of the reference loop (bitwise equal to it) on a slab
 sample of the same instance, all host threads.
 
-N > 1: every rank solves its own seeded instance (replicas, weak scaling; no
-data-path collective -- the slab-sharded single-instance path is SURVEY 8(e)
-and not in this round).  ``--impl reference`` times the CPU reference port on
-rank 0 only; other ranks exit 0.
+N > 1 (torchrun, NCCL): the ONE workload instance is slab-sharded across the
+ranks (paracut_b200.distributed.ShardedAAR): local chain families on a slab
+handle, the cross-slab family on a pencil handle, two NCCL all-to-alls of
+fp32 per iteration ("scaling": "strong", whole-job updates/s).
+``--impl reference`` times the CPU reference port on rank 0 only; other
+ranks exit 0.
 """
 from __future__ import annotations
 
@@ -184,11 +186,110 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, world, rank, local):
+    """N > 1: one instance, slab-sharded over the ranks (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paracut_b200 import _native
+    from paracut_b200.distributed import ShardedAAR, TorchComm
+    from paracut_b200.instances import CONFIGS, make_instance, algorithmic_bytes
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = CONFIGS[args.workload]
+    g = make_instance(spec, seed=args.seed)
+    r, n = len(g.dir_weights), g.n
+    backend = lambda sub: _native.GridSolver(sub, precision="f32", device=local)
+    sh = ShardedAAR(g, TorchComm(), [rank], backend, device="cuda")
+    sh.init_cold()
+    sh.run(args.warmup, norms=False)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    handles = sh.slab + sh.pencil
+    for h in handles:
+        h.reset_launch_count()
+        h.set_profiling(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.15)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    sh.run(args.steps, norms=False)
+    ev1.record()
+    ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    prof = [h.profile_read() for h in handles]
+    launches = sum(h.launch_count() for h in handles)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = r * n * args.steps / (ms_max / 1e3)
+    # dominant family kernel on this rank (slab: local families, pencil: cross)
+    pk, pk_kind = peaks()
+    best = None
+    for h, (fms, fcnt), sub in zip(handles, prof, [sh.geo.slab_grid(g, rank),
+                                                 sh.geo.pencil_grid(g, rank)]):
+        fe = _family_edges(sub)
+        for j in range(len(fms)):
+            if fcnt[j] and (best is None or fms[j] > best[0]):
+                best = (float(fms[j]), int(fcnt[j]), 4 * (2 * sub.n + fe[j]), j)
+    mean_ms = best[0] / best[1]
+    achieved = best[2] / (mean_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
+            "frac": achieved / pk, "traffic": None, "peak_kind": pk_kind,
+            "kernel": "family %d prox sweep (rank %d)" % (best[3], rank),
+            "bytes_per_launch": best[2], "mean_launch_ms": mean_ms}
+    # e2e: build the rank's shards from host arrays, cold start, K steps, read y back
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    sh2 = ShardedAAR(g, TorchComm(), [rank], backend, device="cuda")
+    sh2.init_cold()
+    sh2.run(args.steps, norms=True)
+    ys = sh2.local_shadow()
+    wall = time.perf_counter() - t0
+    wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
+    dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+    wall = float(wt.item())
+    geo = sh.geo
+    h2d = 8 * (geo.n_slab + geo.n_pencil) + 8 * (geo.n_slab * r + geo.n_pencil)
+    d2h = 8 * (geo.n_slab * len(ys[rank][0]) + geo.n_pencil)
+    e2e = {"value": r * n * args.steps / wall, "unit": "updates/s",
+           "h2d_bytes_per_step": world * h2d / args.steps,
+           "d2h_bytes_per_step": world * d2h / args.steps, "wall_s": wall}
+    if rank == 0:
+        B_iter = algorithmic_bytes(g, r, 4)
+        line = {
+            "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32",
+            "arithmetic": "fp32 anchor-relative scan, fp64 drift c and segment values",
+            "data": "synthetic (BASELINE.json generator, seed %d)" % args.seed,
+            "config": {"workload": args.workload, "dims": list(spec.dims),
+                       "connectivity": spec.connectivity, "r": r, "n": n, "precision": "f32",
+                       "step": "1 AAR iteration", "parallelism": "slab%d" % world,
+                       "exchange": "2 x NCCL all-to-all of fp32 per iteration",
+                       "l2": "working set %.0f MB > 126 MB L2, no flush needed"
+                             % (B_iter / 1e6)},
+            "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse_args()
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, world, rank)
+        return
+    if world > 1:
+        run_sharded(args, world, rank, local)
         return
 
     import torch
@@ -293,7 +394,9 @@ def main():
             "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "storage_dtype": "f32" if precision == "f32" else "f64",
+            "dtype": "f32" if precision == "f32" else "f64",
+            "arithmetic": ("fp32 anchor-relative scan, fp64 drift c and segment values"
+                           if precision == "f32" else "fp64, bitwise the reference"),
             "data": "synthetic (BASELINE.json generator, seed %d+rank)" % args.seed,
             "config": {"workload": args.workload, "dims": list(spec.dims),
                        "connectivity": spec.connectivity, "r": r, "n": n,

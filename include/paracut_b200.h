@@ -96,6 +96,27 @@ int pcb_get_z(pcb_solver *h, double *z);
  * out at the end) receives ||z_{k+1} - z_k|| per iteration. */
 int pcb_aar_run(pcb_solver *h, int64_t iters, double *step_norms);
 
+/* Same with step flags (PCB_F32 only), for slab-sharded runs where one
+ * rank's families live on two handles (include the cross-slab family on a
+ * pencil handle): */
+#define PCB_STEP_G_PRESET 1   /* G already holds d of other families: no FIRST role */
+#define PCB_STEP_NO_UPDATE 2  /* no LAST role: drift/primal updated elsewhere      */
+#define PCB_STEP_EXPORT_G 4   /* LAST stores its per-node g = sum_j d_j in G       */
+#define PCB_STEP_NORM_RAW 8   /* step_norms receive sums of squares (partials)    */
+int pcb_aar_step(pcb_solver *h, int64_t iters, int flags, double *step_norms);
+/* Sweep only families whose bit is set (decompose_grid order). */
+int pcb_set_family_mask(pcb_solver *h, unsigned mask);
+/* x -= g; c += (x - g)/r on this handle's nodes, g a device pointer to n
+ * floats (the exported g of the slab side, already in this handle's layout). */
+int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
+/* Device pointer and element count of a handle buffer (for collectives). */
+#define PCB_BUF_G 0      /* float[n] accumulator / exported g */
+#define PCB_BUF_X 1      /* float[n] primal                  */
+#define PCB_BUF_C 2      /* double[n] drift                  */
+#define PCB_BUF_Y 3      /* double[r*n] shadow               */
+#define PCB_BUF_NORMS 4  /* double[] per-iteration norms      */
+int pcb_device_buffer(pcb_solver *h, int which, uintptr_t *ptr, int64_t *count);
+
 /* Shadow y = Pi_K(z) into the handle's shadow buffer (projections.py:89-104);
  * does not change z.  y_out (nullable, r*n) and s_out (nullable, n,
  * aggregate in class order, projections.py:133-137) are copied to host. */

@@ -17,6 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
 
 PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
+STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
+BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
 PRECISIONS = {"f64": 0, "f32": 1}
 
@@ -48,6 +50,10 @@ def _declare(L):
     L.pcb_set_z.argtypes = [P, P]
     L.pcb_get_z.argtypes = [P, P]
     L.pcb_aar_run.argtypes = [P, I64, P]
+    L.pcb_aar_step.argtypes = [P, I64, INT, P]
+    L.pcb_set_family_mask.argtypes = [P, ctypes.c_uint]
+    L.pcb_apply_g.argtypes = [P, ctypes.c_size_t]
+    L.pcb_device_buffer.argtypes = [P, INT, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I64)]
     L.pcb_shadow.argtypes = [P, P, P]
     L.pcb_apply.argtypes = [P, P]
     L.pcb_shadow_get.argtypes = [P, P]
@@ -69,6 +75,7 @@ def _declare(L):
 EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains",
            "pcb_tv1d_prox_batch", "pcb_create", "pcb_destroy", "pcb_shape", "pcb_set_stream",
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
+           "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
            "pcb_get_best", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
@@ -182,6 +189,24 @@ class GridSolver:
         out = np.empty(max(int(iters), 1)) if norms else None
         check(lib().pcb_aar_run(self.handle, int(iters), ptr(out)))
         return out[:int(iters)] if norms else None
+
+    def step(self, iters, flags, norms=True):
+        """pcb_aar_step: fused iterations with sharding flags (STEP_*)."""
+        out = np.empty(max(int(iters), 1)) if norms else None
+        check(lib().pcb_aar_step(self.handle, int(iters), int(flags), ptr(out)))
+        return out[:int(iters)] if norms else None
+
+    def set_family_mask(self, mask):
+        check(lib().pcb_set_family_mask(self.handle, int(mask)))
+
+    def apply_g(self, g_dev_ptr):
+        check(lib().pcb_apply_g(self.handle, int(g_dev_ptr)))
+
+    def device_buffer(self, which):
+        """(device pointer, element count) of a handle buffer (BUF_*)."""
+        p_, n_ = ctypes.c_size_t(0), I64(0)
+        check(lib().pcb_device_buffer(self.handle, int(which), ctypes.byref(p_), ctypes.byref(n_)))
+        return int(p_.value), int(n_.value)
 
     def shadow(self, want_y=False, want_s=False):
         y = np.empty((self.r, self.n)) if want_y else None

@@ -61,6 +61,7 @@ struct Args {
   // pos * 4 + (touch + 1), touch -1 floor / +1 ceiling / 0 piece start; -1 none.
   const int* merge;
   int nb;
+  int export_g;     // LAST: also store the per-node g = sum_j d_j (fp32) in G
 };
 
 __device__ __forceinline__ void cp4(void* dst, const void* src, bool pred) {
@@ -138,11 +139,13 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
   } else if (ROLE == MID) {
     A.G[nd] = (float)((double)A.G[nd] + d);
   } else {
-    const double g = (double)A.G[nd] + d;
+    const float g32 = (float)((double)A.G[nd] + d);
+    const double g = (double)g32;
     const double xn = (double)A.X[nd] - g;
     A.X[nd] = (float)xn;
     const double dcv = (xn - g) * A.inv_r;
     A.c[nd] = cz + dcv;
+    if (A.export_g) A.G[nd] = g32;
     nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
   }
   return nrm;
@@ -279,7 +282,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         const int i = ((lane >> 3) << 3) + ib;
         const int64_t bi = __shfl_sync(0xffffffffu, my_base, i);
         const bool pr = i < nvalid && pos < m;
-        gpre[ib] = pr ? A.G[fam_node(F, bi, pos)] : 0.f;
+        const int64_t nd = pr ? fam_node(F, bi, pos) : 0;
+        gpre[ib] = pr ? A.G[nd] : 0.f;
+        if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : 0.f;
       }
     }
   };
@@ -325,11 +330,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
             } else if (ROLE == MID) {
               A.G[nd] = (float)((double)gpre[q] + d);
             } else {
-              const double g = (double)gpre[q] + d;
+              const float g32 = (float)((double)gpre[q] + d);
+              const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
               A.X[nd] = (float)xn;
               const double dcv = (xn - g) * A.inv_r;
               A.c[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
+              if (A.export_g) A.G[nd] = g32;
               nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
             }
           } else {
@@ -353,9 +360,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         if (has_i && pos >= st_i && pos < sp_i && pos < i0_i) {
           const int ix = rix(i, pos);
           const int64_t nd = fam_node(F, bi, pos);
-          if (ROLE == SHADOW) A.y[nd] = rz[ix];
-          else if (ROLE == FIRST) A.G[nd] = ra[ix];
-          else if (ROLE == MID) A.G[nd] = (float)((double)gpre[ib] + (double)ra[ix]);
+          if (ROLE == SHADOW) {
+            A.y[nd] = rz[ix];
+          } else if (ROLE == FIRST) {
+            A.G[nd] = ra[ix];
+          } else if (ROLE == MID) {
+            A.G[nd] = (float)((double)gpre[ib] + (double)ra[ix]);
+          } else {
+            const float g32 = (float)((double)gpre[ib] + (double)ra[ix]);
+            const double g = (double)g32;
+            const double xn = (double)xpre[ib] - g;
+            A.X[nd] = (float)xn;
+            const double dcv = (xn - g) * A.inv_r;
+            A.c[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
+            if (A.export_g) A.G[nd] = g32;
+            nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
+          }
         }
       }
       __syncwarp();

@@ -720,6 +720,7 @@ struct pcb_solver {
   DBuf<double> sp_cy, sp_fy;
   DBuf<uint8_t> packed;
   int64_t spill_per = 0;  // spill entries per thread
+  unsigned fmask = 0xfu;  // families swept by this handle (sharded runs split them)
   int nbk[MAXR]{};        // fp32 path: blocks per chain (intra-chain split), 1 = whole chains
   int lbk[MAXR]{};        // block length (positions)
   DBuf<int> merge;        // merge points, max_j nbk[j] * C_j
@@ -810,7 +811,8 @@ int setup_geometry(pcb_solver* h) {
     h->fam[2] = mk(K_Z3, (int)D0, D1 * D2, 1, 1, 0, D1 * D2, 0, 0);
     h->r = 3;
   }
-  // fast order: a full-coverage family last (zig-zags leave border singletons)
+  // fast-path order: a row-like family first (its G pass is write-only), a
+  // strided full-coverage family last (zig-zags leave border singletons)
   if (h->r == 4) {
     h->order[0] = 0;
     h->order[1] = 2;
@@ -1000,40 +1002,69 @@ int fam_units(const pcb_solver* h, int j) {
   return (int)((h->fam[j].C + per - 1) / per) * (h->nbk[j] > 1 ? h->nbk[j] : 1);
 }
 
-// one fused fp32 iteration; partials of every family land in parts[], reduced in order
-int step_fast(pcb_solver* h, double* norm_slot) {
+// one fused fp32 iteration over the handle's active families; partials of
+// every family land in parts[], reduced in order.  flags: PCB_STEP_G_PRESET
+// (G already holds other families' d: no FIRST role), PCB_STEP_NO_UPDATE (no
+// LAST role: the drift/primal update happens on another handle),
+// PCB_STEP_EXPORT_G (LAST stores its per-node g in G), PCB_STEP_NORM_RAW
+// (store the sum of squares, not its square root).
+int step_fast(pcb_solver* h, double* norm_slot, int flags) {
   const double inv_r = 1.0 / (double)h->r, rd = (double)h->r;
-  int64_t off = 0;
+  int act[MAXR], na = 0;
   for (int q = 0; q < h->r; ++q) {
     const int j = h->order[q];
+    if (((h->fmask >> j) & 1u) && h->fam[j].C > 0) act[na++] = j;
+  }
+  const bool preset = flags & PCB_STEP_G_PRESET;
+  const bool noupd = flags & PCB_STEP_NO_UPDATE;
+  if (na == 1 && !preset && !noupd) CUDA_TRY(cudaMemsetAsync(h->G32.p, 0, h->n * sizeof(float),
+                                                              h->stream));
+  int64_t off = 0;
+  for (int q = 0; q < na; ++q) {
+    const int j = act[q];
     const Fam& F = h->fam[j];
-    if (F.C == 0) continue;  // only zig-zags can be empty, never first/last
-    const int role = (q == 0) ? pcb::fast::FIRST : (q == h->r - 1 ? pcb::fast::LAST
-                                                                   : pcb::fast::MID);
+    int role;
+    if (q == na - 1 && !noupd) role = pcb::fast::LAST;
+    else if (q == 0 && !preset && !(na == 1 && !noupd)) role = pcb::fast::FIRST;
+    else role = pcb::fast::MID;
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
-                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1};
+                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
+                      (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
     prof_begin(h, j);
     int rc = launch_merge(h, j, a);
     if (!rc) {
       if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a);
       else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a);
-      else rc = launch_sweep<pcb::fast::LAST, false>(h, a);
+      else rc = launch_role<pcb::fast::LAST>(h, a);
     }
     prof_end(h);
     if (rc) return rc;
     off += fam_units(h, j);
   }
-  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot, 1);
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot,
+                                            (flags & PCB_STEP_NORM_RAW) ? 0 : 1);
   LAUNCH_CHECK(h);
   return 0;
+}
+
+// x -= g; c += (x - g) / r on this handle's nodes (the pencil copy of the
+// drift in a sharded run), with g exported by the slab side's LAST family
+__global__ void k_apply_g(const float* g, float* X, double* cdr, int64_t n, double inv_r) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double gv = (double)g[i];
+    const double xn = (double)X[i] - gv;
+    X[i] = (float)xn;
+    cdr[i] += (xn - gv) * inv_r;
+  }
 }
 
 int shadow_fast(pcb_solver* h) {
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
-    if (F.C == 0) continue;
+    if (F.C == 0 || !((h->fmask >> j) & 1u)) continue;
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
-                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p, nullptr, 1};
+                      nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p, nullptr, 1, 0};
     if (int rc = launch_merge(h, j, a)) return rc;
     if (int rc = launch_role<pcb::fast::SHADOW>(h, a)) return rc;
   }
@@ -1247,7 +1278,12 @@ int pcb_get_z(pcb_solver* h, double* z) {
 }
 
 int pcb_aar_run(pcb_solver* h, int64_t iters, double* step_norms) {
+  return pcb_aar_step(h, iters, 0, step_norms);
+}
+
+int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   if (!h) return fail(PCB_E_ARG, "null handle");
+  if (flags && h->precision != PCB_F32) return fail(PCB_E_ARG, "step flags need the f32 path");
   if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
   if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
   if (iters == 0) return 0;
@@ -1260,7 +1296,7 @@ int pcb_aar_run(pcb_solver* h, int64_t iters, double* step_norms) {
       if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
       if ((rc = update_exact(h, h->norms.p + k))) return rc;
     } else {
-      if ((rc = step_fast(h, h->norms.p + k))) return rc;
+      if ((rc = step_fast(h, h->norms.p + k, flags))) return rc;
     }
   }
   h->have_shadow = false;
@@ -1465,6 +1501,37 @@ int pcb_project_K(pcb_solver* h, const double* v, double* out) {
   if (int e = sweep_exact(h, src, dst)) return e;
   CUDA_TRY(cudaMemcpyAsync(out, dst, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_set_family_mask(pcb_solver* h, unsigned mask) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if ((mask & ((1u << h->r) - 1u)) == 0) return fail(PCB_E_ARG, "empty family mask");
+  h->fmask = mask & ((1u << h->r) - 1u);
+  return 0;
+}
+
+int pcb_apply_g(pcb_solver* h, uintptr_t g_dev) {
+  if (!h || !g_dev) return fail(PCB_E_ARG, "null argument");
+  if (h->precision != PCB_F32) return fail(PCB_E_ARG, "apply_g needs the f32 path");
+  if (int e = set_dev(h)) return e;
+  k_apply_g<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+      reinterpret_cast<const float*>(g_dev), h->X32.p, h->cdrift.p, h->n, 1.0 / (double)h->r);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+int pcb_device_buffer(pcb_solver* h, int which, uintptr_t* ptr, int64_t* count) {
+  if (!h || !ptr || !count) return fail(PCB_E_ARG, "null argument");
+  switch (which) {
+    case PCB_BUF_G: *ptr = (uintptr_t)h->G32.p; *count = h->G32.p ? h->n : 0; break;
+    case PCB_BUF_X: *ptr = (uintptr_t)h->X32.p; *count = h->X32.p ? h->n : 0; break;
+    case PCB_BUF_C: *ptr = (uintptr_t)h->cdrift.p; *count = h->cdrift.p ? h->n : 0; break;
+    case PCB_BUF_Y: *ptr = (uintptr_t)h->y.p; *count = (int64_t)h->r * h->n; break;
+    case PCB_BUF_NORMS: *ptr = (uintptr_t)h->norms.p; *count = (int64_t)h->norms.n; break;
+    default: return fail(PCB_E_ARG, "unknown buffer id %d", which);
+  }
+  if (!*ptr) return fail(PCB_E_STATE, "buffer %d not allocated for this precision", which);
   return 0;
 }
 

@@ -1,0 +1,139 @@
+"""Slab-sharded AAR (paracut_b200.distributed): host-side logic on CPU over
+gloo (world 2, CPU emulation of the per-rank kernels), and the real kernels
+with P virtual ranks on one GPU."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paracut_b200.distributed import LocalComm, ShardedAAR, SlabGeometry
+from paracut_b200.instances import CONFIGS, make_instance
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, conn, dims, iters, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import torch.distributed as dist
+    from emu import EmuSolver
+    from paracut_b200.distributed import TorchComm
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = {"2D-4": CONFIGS["cfg2"], "3D-6": CONFIGS["cfg4"]}[conn]
+        g = make_instance(spec, seed=2, dims=dims)
+        sh = ShardedAAR(g, TorchComm(), [rank], EmuSolver)
+        sh.init_cold()
+        norms = sh.run(iters)
+        parts = sh.local_z()
+        ys = sh.local_shadow()
+        q.put((rank, parts, ys, norms))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("conn,dims", [("3D-6", (6, 8, 5)), ("2D-4", (12, 10))])
+def test_gloo_world2_matches_unsharded(conn, dims):
+    import multiprocessing as mp
+    from emu import EmuSolver
+    iters = 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, conn, dims, iters, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    spec = {"2D-4": CONFIGS["cfg2"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=2, dims=dims)
+    ref = EmuSolver(g)
+    ref.init_cold()
+    # unsharded reference in the same family order as the sharded run:
+    # cross family first (FIRST), local families after, LAST = last local one
+    from emu import ORDER
+    cross = {"2D-4": 1, "3D-6": 2}[conn]
+    ORDER_SAVE = ORDER[conn]
+    ORDER[conn] = (cross,) + tuple(j for j in ORDER_SAVE if j != cross)
+    try:
+        ref_norms = ref.run(iters)
+    finally:
+        ORDER[conn] = ORDER_SAVE
+    sh = ShardedAAR.__new__(ShardedAAR)  # only for assemble()
+    from paracut_b200.graph import DIRECTIONS
+    sh.g = g
+    sh.geo = SlabGeometry(g.dims, conn, 2)
+    sh.r = len(DIRECTIONS[conn])
+    sh.cross = cross
+    zparts, yparts = {}, {}
+    for _, parts, ys, _ in res:
+        zparts.update(parts)
+        yparts.update(ys)
+    z = sh.assemble(zparts)
+    y = sh.assemble(yparts)
+    z_ref = ref.get_z()
+    y_ref, _ = ref.shadow()
+    scale = np.max(np.abs(z_ref))
+    assert np.max(np.abs(z - z_ref)) <= 1e-9 * scale
+    assert np.max(np.abs(y - y_ref)) <= 1e-9 * max(1.0, np.max(np.abs(y_ref)))
+    for _, _, _, norms in res:
+        assert np.allclose(norms, ref_norms, rtol=1e-9)
+
+
+def test_geometry_partition():
+    geo = SlabGeometry((8, 6, 4), "3D-6", 4)
+    assert geo.dz == 2 and geo.cp == 6 and geo.n_slab * 4 == 8 * 24
+    g = make_instance(CONFIGS["cfg4"], seed=0, dims=(8, 6, 4))
+    sg = geo.slab_grid(g, 1)
+    assert sg.dims == (2, 6, 4)
+    assert np.array_equal(sg.w, g.w.reshape(8, 24)[2:4].ravel())
+    assert np.array_equal(sg.dir_weights[0], g.dir_weights[0][2:4])
+    pg = geo.pencil_grid(g, 3)
+    assert pg.dims == (8, 1, 6)
+    assert np.array_equal(pg.w, g.w.reshape(8, 24)[:, 18:24].ravel())
+    assert np.array_equal(pg.dir_weights[2].reshape(7, 6), g.dir_weights[2].reshape(7, 24)[:, 18:24])
+    with pytest.raises(ValueError):
+        SlabGeometry((8, 6, 4), "3D-6", 3)
+    with pytest.raises(ValueError):
+        SlabGeometry((8, 8), "2D-8", 2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("conn,dims", [("3D-6", (32, 24, 40)), ("2D-4", (64, 96))])
+def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims):
+    """P slab/pencil handle pairs on one device (LocalComm, no kernel waits on
+    another) reproduce the single-handle f32 run."""
+    import paracut_b200 as pc
+    from paracut_b200 import _native
+    spec = {"2D-4": CONFIGS["cfg2"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=4, dims=dims)
+    k = 25
+    sh = ShardedAAR(g, LocalComm(P), range(P),
+                    lambda sub: _native.GridSolver(sub, precision="f32"), device="cuda")
+    sh.init_cold()
+    norms = sh.run(k)
+    z = sh.assemble(sh.local_z())
+    y = sh.assemble(sh.local_shadow())
+    S = _native.GridSolver(g, precision="f32")
+    S.init_cold()
+    ref_norms = S.run(k)
+    z_ref = S.get_z()
+    y_ref, _ = S.shadow(want_y=True)
+    x = g.w - y.sum(axis=0)
+    x_ref = g.w - y_ref.sum(axis=0)
+    assert np.max(np.abs(x - x_ref)) <= 1e-5 * np.max(np.abs(x_ref))
+    assert np.max(np.abs(z - z_ref)) <= 1e-6 * np.max(np.abs(z_ref))
+    assert np.allclose(norms, ref_norms, rtol=1e-4)
