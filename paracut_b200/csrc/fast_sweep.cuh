@@ -39,7 +39,11 @@ namespace fast {
 constexpr int TP = 8;          // positions per tile
 constexpr int NT = 4;          // tiles in the ring
 constexpr int RL = TP * NT;    // ring length (positions)
-constexpr int WARPS = 4;       // warps per block
+#ifndef PCB_SWEEP_WARPS
+#define PCB_SWEEP_WARPS 4
+#endif
+constexpr int WARPS = PCB_SWEEP_WARPS;  // warps per block (4 x 16 KB rings, 3 blocks/SM; 7 measured slower)
+constexpr int MWARPS = 4;               // warps per block of the merge kernel
 static_assert(RL == 32, "swizzle and start masks assume a 32-position ring");
 static_assert(TP == 8, "mode-B lane mapping assumes 8-position tiles");
 
@@ -621,14 +625,14 @@ constexpr int MW = 16;
 __device__ __forceinline__ int mix(int l, int q) { return l * MW + (q ^ (l & (MW - 1))); }
 
 template <bool ROWLIKE>
-__global__ void __launch_bounds__(WARPS * 32) k_merge(Fam F, const float* p, const float* wf,
+__global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, const float* wf,
                                                       const double* cdr, int lb, int nb, int window,
                                                       int* merge) {
-  __shared__ double sz[WARPS][32 * MW];
-  __shared__ float sa[WARPS][32 * MW];
-  __shared__ float sp[WARPS][32 * MW];
+  __shared__ double sz[MWARPS][32 * MW];
+  __shared__ float sa[MWARPS][32 * MW];
+  __shared__ float sp[MWARPS][32 * MW];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t c0 = ((int64_t)blockIdx.x * WARPS + wib) * 32;
+  const int64_t c0 = ((int64_t)blockIdx.x * MWARPS + wib) * 32;
   const int b = blockIdx.y + 1;
   const int64_t C = F.C;
   const int m = F.m;

@@ -983,7 +983,7 @@ int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) {
   a.nb = 1;
   if (h->nbk[j] <= 1) return 0;
   const Fam& F = h->fam[j];
-  const int per = pcb::fast::WARPS * 32;
+  const int per = pcb::fast::MWARPS * 32;
   const dim3 g((unsigned)((F.C + per - 1) / per), (unsigned)(h->nbk[j] - 1));
   if (fam_rowlike(F.kind))
     pcb::fast::k_merge<true><<<g, per, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
@@ -1184,7 +1184,8 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
     if ((rc = ensure_wf32(h))) return bail(rc);
     if ((rc = choose_split(h))) return bail(rc);
   }
-  if ((rc = ensure_spill(h))) return bail(rc);
+  if (precision == PCB_F64)  // hull spill for the exact kernels (f32 path: lazily, project_K only)
+    if ((rc = ensure_spill(h))) return bail(rc);
   if ((rc = h->bits.alloc(n))) return bail(rc);
   if ((rc = h->xcur.alloc(n))) return bail(rc);
   if ((rc = h->parts.alloc(parts_needed(h)))) return bail(rc);
@@ -1491,6 +1492,7 @@ int pcb_project_K(pcb_solver* h, const double* v, double* out) {
   if (!h || !v || !out) return fail(PCB_E_ARG, "null argument");
   if (int e = set_dev(h)) return e;
   if (int e = ensure_wf64(h)) return e;
+  if (int e = ensure_spill(h)) return e;
   const int64_t rn = (int64_t)h->r * h->n;
   if ((int64_t)h->tmp.n < 2 * rn)
     if (int e = h->tmp.alloc(2 * rn)) return e;
