@@ -46,7 +46,7 @@ CPU_SAMPLE_NODES = 1 << 22
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="cfg4")
@@ -67,47 +67,63 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons; only samples whose timestamp falls
+    inside [mark_start, mark_end] (the timed region) are kept."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "25"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             out, _ = self.proc.communicate(timeout=5)
         except Exception:
             self.proc.kill()
             out, _ = self.proc.communicate()
-        sm, smax, reasons = [], [], set()
+        import datetime
+        sm, smax, reasons, allsm = [], [], set(), []
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
             try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                v, vmax = float(parts[1]), float(parts[2])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
+            allsm.append(v)
+            # keep the timed region, with a 50 ms guard for the sampling period
+            if self.t0 is not None and not (self.t0 - 0.05 <= ts <= self.t1 + 0.05):
+                continue
+            sm.append(v)
+            smax.append(vmax)
+            for nm, flag in zip(names, parts[4:8]):
+                if flag.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
@@ -212,13 +228,15 @@ def run_sharded(args, world, rank, local):
         h.set_profiling(True)
     clocks = ClockSampler(local)
     clocks.start()
-    time.sleep(0.15)
+    time.sleep(0.3)
+    clocks.mark_start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record()
     sh.run(args.steps, norms=False)
     ev1.record()
     ev1.synchronize()
+    clocks.mark_end()
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
     prof = [h.profile_read() for h in handles]
@@ -309,16 +327,16 @@ def main():
     r, n = S.r, S.n
     stream = torch.cuda.Stream(device=local)
     S.set_stream(stream.cuda_stream)
+    clocks = ClockSampler(local)
+    clocks.start()
     S.init_cold()
     S.run(args.warmup, norms=False)
     S.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.15)
+    time.sleep(0.3)
+    clocks.mark_start()
     S.reset_launch_count()
     S.set_profiling(True)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -327,6 +345,7 @@ def main():
     S.run(args.steps, norms=False)
     ev1.record(stream)
     ev1.synchronize()
+    clocks.mark_end()
     ms = ev0.elapsed_time(ev1)
     fam_ms, fam_cnt = S.profile_read()
     S.set_profiling(False)
