@@ -219,6 +219,14 @@ def run_sharded(args, world, rank, local):
     sh = ShardedAAR(g, TorchComm(), [rank], backend, device="cuda")
     sh.init_cold()
     sh.run(args.warmup, norms=False)
+    mode = "cuda-graph"
+    try:
+        sh.capture()  # one iteration as a graph (handles, transposes, NCCL all-to-alls)
+        sh.run_graph(2)
+    except Exception as e:  # capture unsupported here: time the eager loop instead
+        mode = "eager (graph capture failed: %s)" % (str(e).splitlines()[0][:80],)
+        for h in sh.slab + sh.pencil:
+            h.set_stream(0)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -232,9 +240,15 @@ def run_sharded(args, world, rank, local):
     clocks.mark_start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    sh.run(args.steps, norms=False)
-    ev1.record()
+    stream = torch.cuda.current_stream()
+    if mode == "cuda-graph":
+        stream = sh._gstream
+    ev0.record(stream)
+    if mode == "cuda-graph":
+        sh.run_graph(args.steps)
+    else:
+        sh.run(args.steps, norms=False)
+    ev1.record(stream)
     ev1.synchronize()
     clocks.mark_end()
     ms = ev0.elapsed_time(ev1)
@@ -291,6 +305,7 @@ def run_sharded(args, world, rank, local):
                        "connectivity": spec.connectivity, "r": r, "n": n, "precision": "f32",
                        "step": "1 AAR iteration", "parallelism": "slab%d" % world,
                        "exchange": "2 x NCCL all-to-all of fp32 per iteration",
+                       "launch": mode,
                        "l2": "working set %.0f MB > 126 MB L2, no flush needed"
                              % (B_iter / 1e6)},
             "roofline": roof, "cpu_baseline": None, "e2e": e2e, "gpu_launches": launches,

@@ -963,8 +963,14 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
 template <int ROLE, bool ROWLIKE>
 int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
   const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>();
-  CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  // set once per device (outside any later CUDA-graph capture of the sweep)
+  static unsigned set_mask = 0;
+  const unsigned bit = 1u << (h->device & 31);
+  if (!(set_mask & bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    set_mask |= bit;
+  }
   const int per = pcb::fast::WARPS * 32;
   const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
   pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a);

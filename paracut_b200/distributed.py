@@ -249,6 +249,27 @@ class ShardedAAR:
         tot = self.comm.all_sum([a.cpu().numpy() for a in acc])
         return np.sqrt(np.maximum(np.asarray(tot[0], dtype=np.float64), 0.0))
 
+    def capture(self):
+        """Record one fused iteration (norms off) as a CUDA graph; replay it with
+        ``run_graph``.  Every handle launches on the capture stream, torch's
+        transposes and the NCCL all-to-alls are captured with them, so an
+        iteration costs one graph launch on the host."""
+        import torch
+        self.run(1, norms=False)  # warm: lazy setup and attributes outside capture
+        torch.cuda.synchronize()
+        self._gstream = torch.cuda.Stream()
+        for h in self.slab + self.pencil:
+            h.set_stream(self._gstream.cuda_stream)
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph, stream=self._gstream):
+            self.run(1, norms=False)
+        torch.cuda.synchronize()
+        return self._graph
+
+    def run_graph(self, iters):
+        for _ in range(int(iters)):
+            self._graph.replay()
+
     # ---------------------------------------------------------------- results (local ranks)
     def local_z(self):
         """{rank: (slab z of local families [len(LOCAL), n_slab], pencil z_cross [n_pencil])}."""

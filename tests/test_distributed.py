@@ -137,3 +137,33 @@ def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims):
     assert np.max(np.abs(x - x_ref)) <= 1e-5 * np.max(np.abs(x_ref))
     assert np.max(np.abs(z - z_ref)) <= 1e-6 * np.max(np.abs(z_ref))
     assert np.allclose(norms, ref_norms, rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_nccl_world1_and_graph_capture_match_eager():
+    """The TorchComm/NCCL code path (world 1 in-process) and a CUDA-graph
+    capture of one iteration give the same iterates as LocalComm eager."""
+    import torch
+    import torch.distributed as dist
+    from paracut_b200 import _native
+    from paracut_b200.distributed import TorchComm
+    g = make_instance(CONFIGS["cfg4"], seed=6, dims=(16, 20, 24))
+    backend = lambda sub: _native.GridSolver(sub, precision="f32")
+    ref = ShardedAAR(g, LocalComm(1), [0], backend, device="cuda")
+    ref.init_cold()
+    ref.run(12, norms=False)
+    z_ref = ref.assemble(ref.local_z())
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        sh = ShardedAAR(g, TorchComm(), [0], backend, device="cuda")
+        sh.init_cold()
+        sh.run(2, norms=True)
+        sh.capture()          # runs 1 warm iteration, then records one
+        sh.run_graph(9)       # 2 + 1 + 9 = 12 iterations
+        torch.cuda.synchronize()
+        z = sh.assemble(sh.local_z())
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(z, z_ref)

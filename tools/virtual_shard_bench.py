@@ -25,6 +25,13 @@ for P in (1, 2, 4, 8):
     sh.run(20, norms=False)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / 20
-    print("%s P=%d virtual ranks on 1 GPU: %.3f ms/iter (%.2e updates/s)" % (wl, P, dt * 1e3,
-                                                                           r * n / dt))
+    sh.capture()
+    sh.run_graph(3)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh.run_graph(20)
+    torch.cuda.synchronize()
+    dg = (time.perf_counter() - t0) / 20
+    print("%s P=%d virtual ranks on 1 GPU: eager %.3f ms/iter, graph %.3f ms/iter (%.2e updates/s)"
+          % (wl, P, dt * 1e3, dg * 1e3, r * n / dg))
     del sh
