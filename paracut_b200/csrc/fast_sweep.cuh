@@ -44,6 +44,9 @@ constexpr int RL = TP * NT;    // ring length (positions)
 #endif
 constexpr int WARPS = PCB_SWEEP_WARPS;  // warps per block (4 x 16 KB rings, 3 blocks/SM; 7 measured slower)
 constexpr int MWARPS = 4;               // warps per block of the merge kernel
+#ifndef PCB_SCAN_KEEP
+#define PCB_SCAN_KEEP 16  // a round ends when at most this many lanes still have data
+#endif
 static_assert(RL == 32, "swizzle and start masks assume a 32-position ring");
 static_assert(TP == 8, "mode-B lane mapping assumes 8-position tiles");
 
@@ -387,7 +390,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   };
 
   // one round of scanning; LAG: some lane's anchor is below the ring
-  auto scan = [&](int lo_pos, int avail_hi, auto lag_tag) {
+  // keep_min: leave the round once at most this many lanes still have data
+  // (they continue next round), so a few slow lanes do not idle the warp
+  auto scan = [&](int lo_pos, int avail_hi, int keep_min, auto lag_tag) {
     constexpr bool LAG = decltype(lag_tag)::value;
     // software-pipelined ring reads: the next gate's z and a are loaded at the
     // end of the previous trip (slots >= k are never written by the scan)
@@ -395,7 +400,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     float an = ra[rix(lane, k)];
     for (;;) {
       const bool act = !done && k < avail_hi;
-      if (!__any_sync(0xffffffffu, act)) break;
+      if (__popc(__ballot_sync(0xffffffffu, act)) <= keep_min) break;
       if (act) {
         const int kp = k;
         double zabs = zn;
@@ -494,10 +499,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       // One gate per trip.  Warps with no lagging lane (the normal case) run
       // a variant without any below-the-ring checks, with the segment close
       // fully predicated so the warp stays converged through bends.
+      const int keep = (t_rdy < t_ld) ? PCB_SCAN_KEEP : 0;
       if (__any_sync(0xffffffffu, !done && i0 < lo_pos))
-        scan(lo_pos, avail_hi, std::true_type());
+        scan(lo_pos, avail_hi, keep, std::true_type());
       else
-        scan(lo_pos, avail_hi, std::false_type());
+        scan(lo_pos, avail_hi, keep, std::false_type());
       __syncwarp();
       if (__all_sync(0xffffffffu, done)) {
         cp_wait(0);
@@ -508,7 +514,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       // ---------------- retire tiles every lane has emitted
       const int front = __reduce_min_sync(0xffffffffu, done ? 0x7fffffff : i0);
       while (t_lo < t_rdy && (t_lo + 1) * TP <= front) retire(t_lo++);
-      if (t_rdy == t_ld && t_ld - t_lo == NT) retire(t_lo++);  // ring full: lagging lanes go global
+      const bool any_act = __any_sync(0xffffffffu, !done && k < avail_hi);
+      if (!any_act && t_rdy == t_ld && t_ld - t_lo == NT)
+        retire(t_lo++);  // ring full: lagging lanes go global
       __syncwarp();
       while (t_ld < ntiles && t_ld - t_lo < NT) issue(t_ld++);
       if (t_rdy < t_ld) {
