@@ -56,6 +56,7 @@ class SolverConfig:
     precision: str = "f64"
     thresholds: tuple = (0.0,)
     device: int = 0
+    polish_iters: int = 0   # f32 runs that end uncertified: up to this many f64 iterations
 
     def __post_init__(self):
         if self.algorithm not in ALGORITHMS:
@@ -68,6 +69,8 @@ class SolverConfig:
             raise ValueError("threads and check_every must be >= 1")
         if self.precision not in PRECISIONS:
             raise ValueError("precision must be one of %r" % (PRECISIONS,))
+        if self.polish_iters < 0:
+            raise ValueError("polish_iters must be >= 0")
         thr = tuple(float(t) for t in self.thresholds)
         if not 1 <= len(thr) <= MAX_THRESHOLDS:
             raise ValueError("1..%d thresholds supported" % MAX_THRESHOLDS)
@@ -184,6 +187,8 @@ class _Driver:
         self._labs = []
         self.thr = np.asarray(cfg.thresholds, dtype=np.float64)
         self.solver = _native.GridSolver(g, precision=cfg.precision, device=cfg.device)
+        self.best_solver = None
+        self.kmax = cfg.max_iters
         self.t0 = time.perf_counter()
 
     def warm_or_cold(self):
@@ -225,21 +230,22 @@ class _Driver:
             self.best_t = t
             self.best_packed = packed
             self.solver.keep_best(t)
+            self.best_solver = self.solver
         self.iterations = k
         if gap <= self.cfg.gap_tol + GAP_SLACK:
             self.stopped = True
         return self.stopped
 
     def due(self, k):
-        return k % self.cfg.check_every == 0 or k >= self.cfg.max_iters
+        return k % self.cfg.check_every == 0 or k >= self.kmax
 
     def next_due(self, k):
         ce = self.cfg.check_every
-        return min(((k // ce) + 1) * ce, self.cfg.max_iters)
+        return min(((k // ce) + 1) * ce, self.kmax)
 
     def finish(self):
         wall = time.perf_counter() - self.t0
-        lab, x = self.solver.get_best()
+        lab, x = (self.best_solver or self.solver).get_best()
         certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
         if self.cfg.reference is None:
             for row, packed in zip(self.trace, self._labs):
@@ -275,18 +281,32 @@ def solve_aar(g, dec, cfg):
                 break
             have_prev = True
         return drv.finish()
+    k = _loop(drv, S, k)
+    if cfg.precision == "f32" and cfg.polish_iters > 0 and not drv.stopped:
+        # fp32 state leaves a ~1e-5 floor on the discrete gap of large instances;
+        # continue in the exact fp64 mode from the same AAR point to certify
+        S64 = _native.GridSolver(g, precision="f64", device=cfg.device)
+        S64.set_z(S.get_z())
+        drv.solver = S64
+        drv.kmax = k + cfg.polish_iters
+        drv.record("polish_start", k)
+        _loop(drv, S64, k)
+    return drv.finish()
+
+
+def _loop(drv, S, k):
+    """Plain iterations between checks, shadow + certificate + update at checks."""
     while True:
         if drv.due(k):
             S.shadow()
-            if drv.check(k) or k >= cfg.max_iters:
-                break
+            if drv.check(k) or k >= drv.kmax:
+                return k
             drv.record("aar_step_norm", S.apply())
             k += 1
         else:
             nxt = drv.next_due(k)
             drv.record("aar_step_norm", S.run(nxt - k))
             k = nxt
-    return drv.finish()
 
 
 def _not_on_path(name):

@@ -144,3 +144,20 @@ def test_intra_chain_split_matches_oracle(monkeypatch, target, conn, dims):
     x_ref = g.w - y_ref.sum(axis=0)
     x = g.w - res.dual_state.y.sum(axis=0)
     assert _rel(x, x_ref) <= 1e-4
+
+
+def test_integer_full_size_f32_reaches_exact_optimum_and_polish_certifies():
+    """BASELINE cfg2 integer variant (1024^2): the f32 path's labelling has the
+    same (integer) cut energy as the certified fp64 reference-exact run, and a
+    short fp64 polish certifies it."""
+    g = make_instance(CONFIGS["cfg2_int"], seed=0)
+    thr = (0.0, 1e-6, -1e-6, 1e-3, -1e-3)
+    r64 = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=500, check_every=10, gap_tol=1e-6, thresholds=thr))
+    assert r64.certified
+    r32 = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=500, check_every=501, precision="f32",
+                                   thresholds=thr, polish_iters=100))
+    assert r32.certified
+    assert r32.energy == r64.energy
+    assert g.energy(r32.labeling) == r64.energy
