@@ -368,6 +368,7 @@ __global__ void __launch_bounds__(FAM_BLOCK) k_tv1d(const double* s, const doubl
 }  // namespace
 
 #include "fast_sweep.cuh"
+#include "exact_sweep.cuh"
 
 namespace {
 
@@ -901,19 +902,84 @@ int ensure_spill(pcb_solver* h) {
   return 0;
 }
 
-// exact prox of every family: src (r*n) -> dst (r*n)
+template <int RL>
+int launch_exact_sweep(pcb_solver* h, const pcb::exact::ArgSet& S, int nfam, int64_t maxC) {
+  constexpr int bytes = pcb::exact::WARPS * pcb::exact::warp_bytes<RL>();
+  static unsigned set_mask = 0;
+  const unsigned bit = 1u << (h->device & 31);
+  if (!(set_mask & bit)) {
+    CUDA_TRY(cudaFuncSetAttribute(pcb::exact::k_sweep_exact<RL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    set_mask |= bit;
+  }
+  const int per = pcb::exact::WARPS * 32;
+  const dim3 g((unsigned)((maxC + per - 1) / per), (unsigned)nfam);
+  pcb::exact::k_sweep_exact<RL><<<g, per, bytes, h->stream>>>(S);
+  return 0;
+}
+
+// PCB_EXACT_THREAD=1 selects the thread-per-chain kernel (A/B comparisons)
+bool exact_thread_kernel() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PCB_EXACT_THREAD");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// exact prox of every family: src (r*n) -> dst (r*n).  The families are
+// independent and go out as one launch (blockIdx.y = family), except under
+// profiling, where each family is its own launch for per-family timing.
 int sweep_exact(pcb_solver* h, const double* src, double* dst) {
   const Spill sp = spill_of(h);
-  for (int j = 0; j < h->r; ++j) {
-    const Fam& F = h->fam[j];
-    if (F.C == 0) continue;
-    const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
-    prof_begin(h, j);
-    k_family_exact<<<g, FAM_BLOCK, 0, h->stream>>>(F, src + (int64_t)j * h->n,
-                                                    dst + (int64_t)j * h->n, h->wf64[j].p, sp);
-    prof_end(h);
-    LAUNCH_CHECK(h);
+  if (exact_thread_kernel()) {
+    for (int j = 0; j < h->r; ++j) {
+      const Fam& F = h->fam[j];
+      if (F.C == 0) continue;
+      const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
+      prof_begin(h, j);
+      k_family_exact<<<g, FAM_BLOCK, 0, h->stream>>>(F, src + (int64_t)j * h->n,
+                                                      dst + (int64_t)j * h->n, h->wf64[j].p, sp);
+      prof_end(h);
+      LAUNCH_CHECK(h);
+    }
+    return 0;
   }
+  const int64_t gs = ((h->maxC + FAM_BLOCK - 1) / FAM_BLOCK) * FAM_BLOCK;
+  auto args_of = [&](int j) {
+    return pcb::exact::Args{h->fam[j], src + (int64_t)j * h->n, dst + (int64_t)j * h->n,
+                            h->wf64[j].p, sp.cx, sp.cy, sp.fx, sp.fy, gs};
+  };
+  // ring depth from the parallelism on offer (warps per SM over the sweep)
+  int64_t warps = 0;
+  for (int j = 0; j < h->r; ++j) warps += (h->fam[j].C + 31) / 32;
+  const bool deep = warps < 148 * 12;
+  auto launch = [&](const pcb::exact::ArgSet& S, int nfam, int64_t maxC) {
+    return deep ? launch_exact_sweep<32>(h, S, nfam, maxC)
+                : launch_exact_sweep<16>(h, S, nfam, maxC);
+  };
+  if (h->profiling) {
+    for (int j = 0; j < h->r; ++j) {
+      if (h->fam[j].C == 0) continue;
+      pcb::exact::ArgSet S{};
+      S.f[0] = args_of(j);
+      prof_begin(h, j);
+      if (int e = launch(S, 1, h->fam[j].C)) return e;
+      prof_end(h);
+      LAUNCH_CHECK(h);
+    }
+    return 0;
+  }
+  pcb::exact::ArgSet S{};
+  int64_t maxC = 0;
+  for (int j = 0; j < h->r; ++j) {
+    S.f[j] = args_of(j);
+    maxC = h->fam[j].C > maxC ? h->fam[j].C : maxC;
+  }
+  if (maxC == 0) return 0;
+  if (int e = launch(S, h->r, maxC)) return e;
+  LAUNCH_CHECK(h);
   return 0;
 }
 
