@@ -196,14 +196,27 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
     }
   };
 
+  // Hull tops in registers: t1 = entry n-1, t2 = entry n-2 (the anchor when
+  // n == 1), so a push that pops nothing (the common case) touches shared
+  // memory only to store the new entry.  Entry 0 is (c0x, c0y) / (f0x, f0y).
+  int ct1x = 0, ct2x = 0, ft1x = 0, ft2x = 0;
+  double ct1y = 0.0, ct2y = 0.0, ft1y = 0.0, ft2y = 0.0;
+
   auto scan = [&](int lo_pos, int avail_hi, int keep_min) {
+    // software-pipelined ring reads: the next gate's z and weight are loaded
+    // at the end of the previous trip (slots >= k are never written by the scan)
+    double zn = 0.0, an = 0.0;
+    if (!done && k < avail_hi) {
+      zn = s_at(k, lo_pos);
+      an = k < m - 1 ? a_at(k, lo_pos) : 0.0;
+    }
     for (;;) {
       const bool act = !done && k < avail_hi;
       if (__popc(__ballot_sync(0xffffffffu, act)) <= keep_min) break;
       if (!act) continue;
       // ---- one gate of the reference loop (_kernels.py:41-95)
       ++k;
-      const double v = s_at(k - 1, lo_pos);
+      const double v = zn;
       sk += v;
       // the segment sum from the anchor, in the reference's order (a fresh
       // sequential sum from 0.0), kept incrementally: the closing position
@@ -214,28 +227,30 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
       alleq = alleq && (v == ref);
       double rk = 0.0;
       if (k < m) {
-        rk = a_at(k - 1, lo_pos);
+        rk = an;
         if (rk == 0.0) pe = k;
       }
       int bk = -1, bt = 0;
       double by = 0.0;
       const double uy = sk + rk;
       while (nc >= 1) {
-        int px;
-        double py;
-        if (nc >= 2) {
-          px = cx_get(nc - 2);
-          py = cy_get(nc - 2);
-        } else {
-          px = i0;
-          py = a_val;
-        }
-        const int qx = (nc == 1) ? c0x : cx_get(nc - 1);
-        const double qy = (nc == 1) ? c0y : cy_get(nc - 1);
-        if ((qy - py) * (double)(k - qx) >= (uy - qy) * (double)(qx - px))
+        if ((ct1y - ct2y) * (double)(k - ct1x) >= (uy - ct1y) * (double)(ct1x - ct2x)) {
           --nc;
-        else
+          ct1x = ct2x;
+          ct1y = ct2y;
+          if (nc >= 3) {
+            ct2x = cx_get(nc - 2);
+            ct2y = cy_get(nc - 2);
+          } else if (nc == 2) {
+            ct2x = c0x;
+            ct2y = c0y;
+          } else {
+            ct2x = i0;
+            ct2y = a_val;
+          }
+        } else {
           break;
+        }
       }
       c_put(nc, k, uy);
       if (nc == 0) {
@@ -243,7 +258,14 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
         c0y = uy;
         tc0 = tot;
         ec0 = alleq;
+        ct2x = i0;
+        ct2y = a_val;
+      } else {
+        ct2x = ct1x;
+        ct2y = ct1y;
       }
+      ct1x = k;
+      ct1y = uy;
       ++nc;
       if (nf >= 1 && (c0y - a_val) * (double)(f0x - i0) < (f0y - a_val) * (double)(c0x - i0)) {
         bk = f0x;
@@ -252,21 +274,23 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
       } else {
         const double ly = sk - rk;
         while (nf >= 1) {
-          int px;
-          double py;
-          if (nf >= 2) {
-            px = fx_get(nf - 2);
-            py = fy_get(nf - 2);
-          } else {
-            px = i0;
-            py = a_val;
-          }
-          const int qx = (nf == 1) ? f0x : fx_get(nf - 1);
-          const double qy = (nf == 1) ? f0y : fy_get(nf - 1);
-          if ((qy - py) * (double)(k - qx) <= (ly - qy) * (double)(qx - px))
+          if ((ft1y - ft2y) * (double)(k - ft1x) <= (ly - ft1y) * (double)(ft1x - ft2x)) {
             --nf;
-          else
+            ft1x = ft2x;
+            ft1y = ft2y;
+            if (nf >= 3) {
+              ft2x = fx_get(nf - 2);
+              ft2y = fy_get(nf - 2);
+            } else if (nf == 2) {
+              ft2x = f0x;
+              ft2y = f0y;
+            } else {
+              ft2x = i0;
+              ft2y = a_val;
+            }
+          } else {
             break;
+          }
         }
         f_put(nf, k, ly);
         if (nf == 0) {
@@ -274,7 +298,14 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
           f0y = ly;
           tf0 = tot;
           ef0 = alleq;
+          ft2x = i0;
+          ft2y = a_val;
+        } else {
+          ft2x = ft1x;
+          ft2y = ft1y;
         }
+        ft1x = k;
+        ft1y = ly;
         ++nf;
         if ((f0y - a_val) * (double)(c0x - i0) > (c0y - a_val) * (double)(f0x - i0)) {
           bk = c0x;
@@ -298,46 +329,51 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
           }
         }
       }
-      if (bk < 0) continue;
-      // ---- close [i0, bk): fresh sum + tube offsets (_kernels.py:116-137)
-      const double stot = (bk == k) ? tot : (bk == c0x) ? tc0 : tf0;
-      const bool seq = (bk == k) ? alleq : (bk == c0x) ? ec0 : ef0;
-      double corr = 0.0;
-      const double abk = (bt != 0) ? a_at(bk - 1, lo_pos) : 0.0;
-      if (bt != 0) corr += (double)bt * abk;
-      if (a_t != 0) corr -= (double)a_t * a_im1;
-      const double fill = (seq && corr == 0.0) ? ref : (stot + corr) / (double)(bk - i0);
-      int e2 = i0;
-      if (i0 < lo_pos) {
-        // lagging lane (anchor below the ring): positions below go straight out
-        e2 = min(bk, lo_pos);
-        for (int j = i0; j < e2; ++j) {
-          const int64_t nd = fam_node(F, my_base, j);
-          A.y[nd] = A.z[nd] - fill;
+      if (bk >= 0) {
+        // ---- close [i0, bk) (_kernels.py:116-137)
+        const double stot = (bk == k) ? tot : (bk == c0x) ? tc0 : tf0;
+        const bool seq = (bk == k) ? alleq : (bk == c0x) ? ec0 : ef0;
+        double corr = 0.0;
+        const double abk = (bt != 0) ? a_at(bk - 1, lo_pos) : 0.0;
+        if (bt != 0) corr += (double)bt * abk;
+        if (a_t != 0) corr -= (double)a_t * a_im1;
+        const double fill = (seq && corr == 0.0) ? ref : (stot + corr) / (double)(bk - i0);
+        int e2 = i0;
+        if (i0 < lo_pos) {
+          // lagging lane (anchor below the ring): positions below go straight out
+          e2 = min(bk, lo_pos);
+          for (int j = i0; j < e2; ++j) {
+            const int64_t nd = fam_node(F, my_base, j);
+            A.y[nd] = A.z[nd] - fill;
+          }
         }
+        if (e2 < bk) {
+          ra[rix(lane, e2)] = fill;  // weight slot of e2 is dead from here: holds the value
+          smask |= 1u << (e2 & (RL - 1));
+        }
+        i0 = bk;
+        if (i0 == pe) {
+          a_val = 0.0;
+          a_t = 0;
+          a_S = 0.0;
+          pe = m;
+          done = i0 >= m;
+        } else {
+          a_val = by;
+          a_t = bt;
+          a_S = (bt == 0) ? by : by - (double)bt * abk;
+        }
+        a_im1 = abk;
+        k = i0;
+        sk = a_S;
+        tot = 0.0;
+        alleq = true;
+        nc = nf = 0;
       }
-      if (e2 < bk) {
-        ra[rix(lane, e2)] = fill;  // weight slot of e2 is dead from here: holds the value
-        smask |= 1u << (e2 & (RL - 1));
+      if (!done && k < avail_hi) {
+        zn = s_at(k, lo_pos);
+        an = k < m - 1 ? a_at(k, lo_pos) : 0.0;
       }
-      i0 = bk;
-      if (i0 == pe) {
-        a_val = 0.0;
-        a_t = 0;
-        a_S = 0.0;
-        pe = m;
-        done = i0 >= m;
-      } else {
-        a_val = by;
-        a_t = bt;
-        a_S = (bt == 0) ? by : by - (double)bt * abk;
-      }
-      a_im1 = abk;
-      k = i0;
-      sk = a_S;
-      tot = 0.0;
-      alleq = true;
-      nc = nf = 0;
     }
   };
 
