@@ -145,6 +145,16 @@ int pcb_get_check(pcb_solver *h, int t, uint8_t *labels, int packed, double *x);
 int pcb_keep_best(pcb_solver *h, int t);
 int pcb_get_best(pcb_solver *h, uint8_t *labels, double *x);
 
+/* Best level set of a TV solution (best_level_set_gap, certify.py:50-65 over
+ * solvers.level_sets, solvers.py:86-97): of the labelings {x > v}, v over the
+ * distinct values of x, and the all-ones labeling, the one of least energy
+ * (hence least gap for any dual).  x: host fp64[n], or NULL for the x of the
+ * current check.  *u receives v (-inf for all ones): the labeling is
+ * x > *u, so pcb_check with threshold *u certifies it with the deterministic
+ * reductions.  *energy (nullable) receives its energy from the one-sort scan
+ * (fp64 atomics: exact for integer weights, last-bit rounding otherwise). */
+int pcb_level_set(pcb_solver *h, const double *x, double *u, double *energy);
+
 /* Pi_K of an arbitrary r*n host vector with this grid's decomposition
  * (project_K, projections.py:89-104); fp64 exact kernels regardless of the
  * handle precision. */

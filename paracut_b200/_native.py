@@ -62,6 +62,7 @@ def _declare(L):
     L.pcb_get_check.argtypes = [P, INT, P, INT, P]
     L.pcb_keep_best.argtypes = [P, INT]
     L.pcb_get_best.argtypes = [P, P, P]
+    L.pcb_level_set.argtypes = [P, P, P, P]
     L.pcb_project_K.argtypes = [P, P, P]
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
     L.pcb_set_profiling.argtypes = [P, INT]
@@ -77,7 +78,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
-           "pcb_get_best", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_get_best", "pcb_level_set", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
 
 
@@ -255,6 +256,20 @@ class GridSolver:
         x = np.empty(self.n)
         check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
         return lab, x
+
+    def level_set(self, x=None):
+        """Best level set {x > u} of x (host array) or of the current check's x.
+
+        Returns (u, energy); u = -inf for the all-ones labeling.
+        """
+        xa = None
+        if x is not None:
+            xa = _f64(x)
+            if xa.shape != (self.n,):
+                raise ValueError("length mismatch")
+        u, e = ctypes.c_double(0.0), ctypes.c_double(0.0)
+        check(lib().pcb_level_set(self.handle, ptr(xa), ctypes.byref(u), ctypes.byref(e)))
+        return float(u.value), float(e.value)
 
     def project_K(self, v):
         v = _f64(v)

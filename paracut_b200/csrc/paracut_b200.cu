@@ -1182,6 +1182,8 @@ int parts_needed(const pcb_solver* h) {
 
 }  // namespace
 
+#include "level_sets.cuh"
+
 // =================================================================== C ABI
 
 extern "C" {
@@ -1557,6 +1559,87 @@ int pcb_get_best(pcb_solver* h, uint8_t* labels, double* x) {
     CUDA_TRY(cudaMemcpyAsync(x, h->bestx.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
                              h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_level_set(pcb_solver* h, const double* x, double* u, double* energy) {
+  if (!h || !u) return fail(PCB_E_ARG, "null argument");
+  if (!x && !h->have_check) return fail(PCB_E_STATE, "no current check (pass x or call pcb_check)");
+  if (h->n >= ((int64_t)1 << 31) - 2) return fail(PCB_E_ARG, "level sets: n must be < 2^31");
+  if (int e = set_dev(h)) return e;
+  namespace L = pcb::levels;
+  const int64_t n = h->n;
+  const int ni = (int)n;
+  cudaStream_t st = h->stream;
+  DBuf<double> xin, xs, ws, wp, diff, cutp, E, out;
+  DBuf<int> idx0, idx, flag, rs, rank_of;
+  DBuf<int64_t> last_of;
+  DBuf<L::ArgMin> parts;
+  DBuf<unsigned char> tmp;
+  const double* xd = h->xcur.p;
+  if (x) {
+    if (int e = xin.alloc(n)) return e;
+    CUDA_TRY(cudaMemcpyAsync(xin.p, x, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    xd = xin.p;
+  }
+  if (int e = xs.alloc(n)) return e;
+  if (int e = idx0.alloc(n)) return e;
+  if (int e = idx.alloc(n)) return e;
+  const int g = grid_for(n, 256, NODE_GRID);
+  L::k_iota<<<g, 256, 0, st>>>(idx0.p, n);
+  LAUNCH_CHECK(h);
+  size_t need = 0, b2 = 0;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, need, xd, xs.p, idx0.p, idx.p, ni, 0, 64, st));
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, b2, xs.p, ws.p, ni, st));
+  need = need > b2 ? need : b2;
+  if (int e = tmp.alloc(need)) return e;
+  size_t bytes = need;
+  CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, xd, xs.p, idx0.p, idx.p, ni, 0, 64, st));
+  idx0.free();
+  if (int e = flag.alloc(n)) return e;
+  if (int e = rs.alloc(n)) return e;
+  L::k_flags<<<g, 256, 0, st>>>(xs.p, n, flag.p);
+  LAUNCH_CHECK(h);
+  bytes = need;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp.p, bytes, flag.p, rs.p, ni, st));
+  flag.free();
+  int K = 0;
+  CUDA_TRY(cudaMemcpyAsync(&K, rs.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (int e = rank_of.alloc(n)) return e;
+  if (int e = ws.alloc(n)) return e;
+  if (int e = last_of.alloc((size_t)K + 1)) return e;
+  L::k_scatter_ranks<<<g, 256, 0, st>>>(rs.p, idx.p, h->w.p, n, rank_of.p, ws.p, last_of.p);
+  LAUNCH_CHECK(h);
+  if (int e = diff.alloc((size_t)K + 2)) return e;
+  CUDA_TRY(cudaMemsetAsync(diff.p, 0, ((size_t)K + 2) * sizeof(double), st));
+  DirPtrs dp{};
+  for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
+  L::k_cut_diff<<<g, 256, 0, st>>>(h->D, h->DG, dp, rank_of.p, diff.p);
+  LAUNCH_CHECK(h);
+  if (int e = cutp.alloc((size_t)K + 1)) return e;
+  if (int e = wp.alloc(n)) return e;
+  bytes = need;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp.p, bytes, diff.p, cutp.p, K + 1, st));
+  bytes = need;
+  CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp.p, bytes, ws.p, wp.p, ni, st));
+  if (int e = E.alloc((size_t)K + 1)) return e;
+  L::k_energies<<<grid_for(K + 1, 256, NODE_GRID), 256, 0, st>>>(cutp.p, wp.p, last_of.p, K, n,
+                                                                 E.p);
+  LAUNCH_CHECK(h);
+  constexpr int AB = 256;
+  const int ga = grid_for(K + 1, AB, 148 * 2);
+  if (int e = parts.alloc(ga)) return e;
+  if (int e = out.alloc(3)) return e;
+  L::k_argmin<<<ga, AB, 0, st>>>(E.p, K + 1, parts.p);
+  LAUNCH_CHECK(h);
+  L::k_argmin_final<<<1, 1, 0, st>>>(parts.p, ga, xs.p, last_of.p, out.p);
+  LAUNCH_CHECK(h);
+  double hv[3];
+  CUDA_TRY(cudaMemcpyAsync(hv, out.p, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *u = hv[0];
+  if (energy) *energy = hv[1];
   return 0;
 }
 

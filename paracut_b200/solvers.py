@@ -18,7 +18,9 @@ computes every prox in fp64 -- the fast path for large grids.
 Extensions (defaults give the reference's behaviour): ``thresholds`` lists
 extra primal thresholds evaluated in the same pass; each check keeps the
 smallest-gap one (ties -> earlier entry), which certifies integer instances
-with exact-zero plateaus.  The algorithms "bcd", "ap" and
+with exact-zero plateaus; ``level_sets=True`` adds, at
+every check, the best level set of x (best_level_set_gap, certify.py:50-65,
+as one device sort), which is never worse than any threshold.  The algorithms "bcd", "ap" and
 "fista" are accepted by ``SolverConfig`` for compatibility but are outside
 this path and raise NotImplementedError in ``solve``.
 """
@@ -57,6 +59,7 @@ class SolverConfig:
     thresholds: tuple = (0.0,)
     device: int = 0
     polish_iters: int = 0   # f32 runs that end uncertified: up to this many f64 iterations
+    level_sets: bool = False  # each check also tries the best level set of x (on the device)
 
     def __post_init__(self):
         if self.algorithm not in ALGORITHMS:
@@ -74,6 +77,9 @@ class SolverConfig:
         thr = tuple(float(t) for t in self.thresholds)
         if not 1 <= len(thr) <= MAX_THRESHOLDS:
             raise ValueError("1..%d thresholds supported" % MAX_THRESHOLDS)
+        if self.level_sets and len(thr) >= MAX_THRESHOLDS:
+            raise ValueError("level_sets needs a free threshold slot (<= %d thresholds)"
+                             % (MAX_THRESHOLDS - 1))
         self.thresholds = thr
 
 
@@ -181,6 +187,7 @@ class _Driver:
         self.best_gap = np.inf
         self.best_energy = np.nan
         self.best_t = 0
+        self.best_thr = float(cfg.thresholds[0])
         self.best_packed = None
         self.iterations = 0
         self.stopped = False
@@ -212,7 +219,15 @@ class _Driver:
         self.monitor.setdefault(name, []).extend(float(v) for v in np.atleast_1d(values))
 
     def check(self, k):
-        energies, gaps, dual = self.solver.check(self.thr)
+        thr = self.thr
+        energies, gaps, dual = self.solver.check(thr)
+        if self.cfg.level_sets:
+            # best level set of this x (one device sort), certified by a second
+            # pass of the same deterministic reductions as the thresholds
+            u, _ = self.solver.level_set()
+            if not np.any(thr == u):
+                thr = np.append(thr, u)
+                energies, gaps, dual = self.solver.check(thr)
         t = int(np.argmin(gaps))  # first minimum: threshold 0 wins ties
         gap, en = float(gaps[t]), float(energies[t])
         jac = np.nan
@@ -228,6 +243,7 @@ class _Driver:
             self.best_gap = gap
             self.best_energy = en
             self.best_t = t
+            self.best_thr = float(thr[t])
             self.best_packed = packed
             self.solver.keep_best(t)
             self.best_solver = self.solver
@@ -255,7 +271,7 @@ class _Driver:
                            gap=self.best_gap, iterations=self.iterations, certified=certified,
                            dual_state=state, trace=self.trace, wall_time=wall,
                            algorithm=self.cfg.algorithm, monitor=self.monitor,
-                           threshold=float(self.thr[self.best_t]))
+                           threshold=self.best_thr)
 
 
 def solve_aar(g, dec, cfg):

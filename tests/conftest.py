@@ -44,3 +44,7 @@ def oracle_lib():
     from oracle import oracle as orc
     orc.lib()
     return orc
+
+
+def level_cases():
+    return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "levels_*.npz")))

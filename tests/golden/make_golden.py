@@ -218,6 +218,39 @@ def main():
     d.update(labeling=lab, energy=np.array(e))
     save("kat.npz", **d)
 
+    make_levels()
 
-if __name__ == "__main__":
+
+def make_levels():
+    """Best-level-set certificates (certify.py:50-65) on partially solved x."""
+    global _PC
+    pc = import_reference()
+    _PC = pc
+    sys.path.insert(0, REPO)
+    from paracut_b200.instances import synth_image, energy_from_image
+    r = np.random.default_rng(9)
+    cases = [("r2d4", pc.random_grid((12, 10), "2D-4", r), 3),
+             ("r2d8", pc.random_grid((9, 11), "2D-8", r), 4),
+             ("r3d6", pc.random_grid((4, 5, 6), "3D-6", r), 2)]
+    for conn, dims in (("2D-4", (24, 20)), ("3D-6", (6, 7, 5))):
+        ours = energy_from_image(synth_image(dims, 3, 2, 6, seed=11), conn, integer=True)
+        cases.append(("i" + conn.replace("-", "").lower(),
+                      pc.GridEnergy(ours.dims, conn, ours.w, ours.dir_weights), 5))
+    for name, g, iters in cases:
+        res = pc.solve(g, pc.decompose_grid(g),
+                       pc.SolverConfig(algorithm="aar", max_iters=iters, check_every=iters + 1))
+        s = res.dual_state.y.sum(axis=0)
+        x = g.w - s
+        lab, cert = pc.best_level_set_gap(g, x, s)
+        base = pc.discrete_gap(g, pc.threshold(x), s)
+        d = grid_arrays(g)
+        d.update(x=x, s=s, labeling=lab, gap=np.array(cert.gap),
+                 energy=np.array(cert.primal_energy), dual=np.array(cert.dual_objective),
+                 thr0_gap=np.array(base.gap), nlevels=np.array(len(pc.level_sets(x))))
+        save("levels_%s.npz" % name, **d)
+
+
+if __name__ == "__main__" and "levels" in sys.argv[1:]:
+    make_levels()
+elif __name__ == "__main__":
     main()
