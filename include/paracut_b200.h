@@ -145,6 +145,24 @@ int pcb_get_check(pcb_solver *h, int t, uint8_t *labels, int packed, double *x);
 int pcb_keep_best(pcb_solver *h, int t);
 int pcb_get_best(pcb_solver *h, uint8_t *labels, double *x);
 
+/* The reference's other dual schemes on the same kernels (fp64 handles;
+ * iterates bitwise equal to the reference):
+ *   PCB_ALG_BCD   solve_bcd   solvers.py:212-243  cyclic block projections
+ *   PCB_ALG_AP    solve_ap    solvers.py:246-269  alternating projections
+ *   PCB_ALG_FISTA solve_fista solvers.py:310-341  accelerated projected gradient
+ * pcb_dual_init sets the iterate y (host r*n, or NULL for zeros; FISTA also
+ * v = y, t = 1).  pcb_dual_run performs `iters` iterations; monitor[k]
+ * (nullable) receives the reference's per-iteration monitor value (BCD and
+ * FISTA: "dual_objective", AP: "ap_distance") and stop[k] (nullable) the
+ * dual_tol quantity (BCD: sqrt(change2), AP: |y - yprev|, FISTA: |dy|).
+ * Afterwards pcb_check / pcb_shadow_get read y, and pcb_get_z reads lam (AP)
+ * or v (FISTA).  pcb_init_cold / pcb_set_z return the handle to AAR. */
+#define PCB_ALG_BCD 1
+#define PCB_ALG_AP 2
+#define PCB_ALG_FISTA 3
+int pcb_dual_init(pcb_solver *h, int alg, const double *y0);
+int pcb_dual_run(pcb_solver *h, int64_t iters, double *monitor, double *stop);
+
 /* Best level set of a TV solution (best_level_set_gap, certify.py:50-65 over
  * solvers.level_sets, solvers.py:86-97): of the labelings {x > v}, v over the
  * distinct values of x, and the all-ones labeling, the one of least energy

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
 PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
 BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
+ALG_BCD, ALG_AP, ALG_FISTA = 1, 2, 3
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
 PRECISIONS = {"f64": 0, "f32": 1}
 
@@ -63,6 +64,8 @@ def _declare(L):
     L.pcb_keep_best.argtypes = [P, INT]
     L.pcb_get_best.argtypes = [P, P, P]
     L.pcb_level_set.argtypes = [P, P, P, P]
+    L.pcb_dual_init.argtypes = [P, INT, P]
+    L.pcb_dual_run.argtypes = [P, I64, P, P]
     L.pcb_project_K.argtypes = [P, P, P]
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
     L.pcb_set_profiling.argtypes = [P, INT]
@@ -78,7 +81,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
-           "pcb_get_best", "pcb_level_set", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
 
 
@@ -256,6 +259,22 @@ class GridSolver:
         x = np.empty(self.n)
         check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
         return lab, x
+
+    def dual_init(self, alg, y0=None):
+        """Start a BCD/AP/FISTA iterate (ALG_*) from y0 (r, n) or zeros."""
+        ya = None
+        if y0 is not None:
+            ya = _f64(y0)
+            if ya.shape != (self.r, self.n):
+                raise ValueError("expected shape %r" % ((self.r, self.n),))
+        check(lib().pcb_dual_init(self.handle, int(alg), ptr(ya)))
+
+    def dual_run(self, iters, stop=False):
+        """iters scheme iterations -> (monitor[iters], stop quantity[iters] or None)."""
+        mon = np.empty(max(int(iters), 0))
+        st = np.empty_like(mon) if stop else None
+        check(lib().pcb_dual_run(self.handle, int(iters), ptr(mon), ptr(st)))
+        return mon, st
 
     def level_set(self, x=None):
         """Best level set {x > u} of x (host array) or of the current check's x.

@@ -696,6 +696,8 @@ struct pcb_solver {
   bool y_valid = false;  // y holds the last shadow (not clobbered by aar_run)
   bool have_check = false;
   bool have_best = false;
+  int alg = 0;            // 0: AAR state; PCB_ALG_*: a dual scheme owns y/z
+  double fista_t = 1.0;   // FISTA momentum parameter t_k
   int check_T = 0;
 
   DBuf<double> w;
@@ -928,19 +930,27 @@ bool exact_thread_kernel() {
   return v == 1;
 }
 
-// exact prox of every family: src (r*n) -> dst (r*n).  The families are
-// independent and go out as one launch (blockIdx.y = family), except under
-// profiling, where each family is its own launch for per-family timing.
-int sweep_exact(pcb_solver* h, const double* src, double* dst) {
+// exact prox of families j0..j1-1: srcs[j-j0] -> dsts[j-j0] (n each).  The
+// families are independent and go out as one launch (blockIdx.y = family),
+// except under profiling, where each family is its own launch for
+// per-family timing.
+int sweep_exact_sel(pcb_solver* h, int j0, int j1, const double* const* srcs,
+                    double* const* dsts, bool zero_singletons = false) {
   const Spill sp = spill_of(h);
+  // a zig-zag family leaves border nodes as one-node chains (y = 0 there,
+  // decompose.py:153-183) that no kernel writes: clear them in a fresh dst
+  if (zero_singletons)
+    for (int j = j0; j < j1; ++j)
+      if (h->fam[j].kind == K_ZZ0 || h->fam[j].kind == K_ZZ1)
+        CUDA_TRY(cudaMemsetAsync(dsts[j - j0], 0, h->n * sizeof(double), h->stream));
   if (exact_thread_kernel()) {
-    for (int j = 0; j < h->r; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const Fam& F = h->fam[j];
       if (F.C == 0) continue;
       const int g = (int)((F.C + FAM_BLOCK - 1) / FAM_BLOCK);
       prof_begin(h, j);
-      k_family_exact<<<g, FAM_BLOCK, 0, h->stream>>>(F, src + (int64_t)j * h->n,
-                                                      dst + (int64_t)j * h->n, h->wf64[j].p, sp);
+      k_family_exact<<<g, FAM_BLOCK, 0, h->stream>>>(F, srcs[j - j0], dsts[j - j0], h->wf64[j].p,
+                                                      sp);
       prof_end(h);
       LAUNCH_CHECK(h);
     }
@@ -948,19 +958,20 @@ int sweep_exact(pcb_solver* h, const double* src, double* dst) {
   }
   const int64_t gs = ((h->maxC + FAM_BLOCK - 1) / FAM_BLOCK) * FAM_BLOCK;
   auto args_of = [&](int j) {
-    return pcb::exact::Args{h->fam[j], src + (int64_t)j * h->n, dst + (int64_t)j * h->n,
-                            h->wf64[j].p, sp.cx, sp.cy, sp.fx, sp.fy, gs};
+    return pcb::exact::Args{h->fam[j],   srcs[j - j0], dsts[j - j0], h->wf64[j].p,
+                            sp.cx,       sp.cy,        sp.fx,        sp.fy,
+                            gs};
   };
   // ring depth from the parallelism on offer (warps per SM over the sweep)
   int64_t warps = 0;
-  for (int j = 0; j < h->r; ++j) warps += (h->fam[j].C + 31) / 32;
+  for (int j = j0; j < j1; ++j) warps += (h->fam[j].C + 31) / 32;
   const bool deep = warps < 148 * 12;
   auto launch = [&](const pcb::exact::ArgSet& S, int nfam, int64_t maxC) {
     return deep ? launch_exact_sweep<32>(h, S, nfam, maxC)
                 : launch_exact_sweep<16>(h, S, nfam, maxC);
   };
   if (h->profiling) {
-    for (int j = 0; j < h->r; ++j) {
+    for (int j = j0; j < j1; ++j) {
       if (h->fam[j].C == 0) continue;
       pcb::exact::ArgSet S{};
       S.f[0] = args_of(j);
@@ -973,14 +984,25 @@ int sweep_exact(pcb_solver* h, const double* src, double* dst) {
   }
   pcb::exact::ArgSet S{};
   int64_t maxC = 0;
-  for (int j = 0; j < h->r; ++j) {
-    S.f[j] = args_of(j);
+  for (int j = j0; j < j1; ++j) {
+    S.f[j - j0] = args_of(j);
     maxC = h->fam[j].C > maxC ? h->fam[j].C : maxC;
   }
   if (maxC == 0) return 0;
-  if (int e = launch(S, h->r, maxC)) return e;
+  if (int e = launch(S, j1 - j0, maxC)) return e;
   LAUNCH_CHECK(h);
   return 0;
+}
+
+// exact prox of every family: src (r*n) -> dst (r*n), y_j = z_j - prox(z_j)
+int sweep_exact(pcb_solver* h, const double* src, double* dst, bool zero_singletons = false) {
+  const double* srcs[MAXR];
+  double* dsts[MAXR];
+  for (int j = 0; j < h->r; ++j) {
+    srcs[j] = src + (int64_t)j * h->n;
+    dsts[j] = dst + (int64_t)j * h->n;
+  }
+  return sweep_exact_sel(h, 0, h->r, srcs, dsts, zero_singletons);
 }
 
 constexpr int NODE_GRID = 148 * 8;
@@ -1180,6 +1202,8 @@ int parts_needed(const pcb_solver* h) {
   return (int)need;
 }
 
+#include "dual_schemes.cuh"
+
 }  // namespace
 
 #include "level_sets.cuh"
@@ -1311,6 +1335,7 @@ int pcb_init_cold(pcb_solver* h) {
   LAUNCH_CHECK(h);
   h->have_state = true;
   h->have_shadow = false;
+  h->alg = 0;
   return 0;
 }
 
@@ -1330,6 +1355,7 @@ int pcb_set_z(pcb_solver* h, const double* z) {
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->have_state = true;
   h->have_shadow = false;
+  h->alg = 0;
   return 0;
 }
 
@@ -1358,6 +1384,7 @@ int pcb_aar_run(pcb_solver* h, int64_t iters, double* step_norms) {
 
 int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   if (!h) return fail(PCB_E_ARG, "null handle");
+  if (h->alg) return fail(PCB_E_STATE, "handle holds a dual-scheme state (init_cold/set_z for AAR)");
   if (flags && h->precision != PCB_F32) return fail(PCB_E_ARG, "step flags need the f32 path");
   if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
   if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
@@ -1386,6 +1413,7 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
 
 int pcb_shadow(pcb_solver* h, double* y_out, double* s_out) {
   if (!h) return fail(PCB_E_ARG, "null handle");
+  if (h->alg) return fail(PCB_E_STATE, "handle holds a dual-scheme state (init_cold/set_z for AAR)");
   if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
   if (int e = set_dev(h)) return e;
   int rc;
@@ -1448,6 +1476,7 @@ int pcb_shadow_delta(pcb_solver* h, double* delta) {
 
 int pcb_apply(pcb_solver* h, double* step_norm) {
   if (!h) return fail(PCB_E_ARG, "null handle");
+  if (h->alg) return fail(PCB_E_STATE, "handle holds a dual-scheme state (init_cold/set_z for AAR)");
   if (!h->have_shadow) return fail(PCB_E_STATE, "apply needs a current shadow (call pcb_shadow)");
   if (int e = set_dev(h)) return e;
   int rc;
@@ -1558,6 +1587,69 @@ int pcb_get_best(pcb_solver* h, uint8_t* labels, double* x) {
   if (x)
     CUDA_TRY(cudaMemcpyAsync(x, h->bestx.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
                              h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_dual_init(pcb_solver* h, int alg, const double* y0) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (alg != PCB_ALG_BCD && alg != PCB_ALG_AP && alg != PCB_ALG_FISTA)
+    return fail(PCB_E_ARG, "unknown dual scheme %d", alg);
+  if (h->precision != PCB_F64) return fail(PCB_E_ARG, "dual schemes run on fp64 handles");
+  if (int e = set_dev(h)) return e;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (y0)
+    CUDA_TRY(cudaMemcpyAsync(h->y.p, y0, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  else
+    CUDA_TRY(cudaMemsetAsync(h->y.p, 0, rn * sizeof(double), h->stream));
+  if (alg == PCB_ALG_FISTA)  // v = y.copy()
+    CUDA_TRY(cudaMemcpyAsync(h->z.p, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToDevice,
+                             h->stream));
+  const size_t need = (size_t)(alg == PCB_ALG_BCD ? 3 * h->n : 2 * rn);
+  if (h->tmp.n < need)
+    if (int e = h->tmp.alloc(need)) return e;
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->alg = alg;
+  h->fista_t = 1.0;
+  h->have_state = true;
+  h->have_shadow = true;  // y is the iterate pcb_check certifies
+  h->y_valid = true;
+  h->have_check = false;
+  return 0;
+}
+
+int pcb_dual_run(pcb_solver* h, int64_t iters, double* monitor, double* stop) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->alg) return fail(PCB_E_STATE, "no dual scheme state (call pcb_dual_init)");
+  if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
+  if (iters == 0) return 0;
+  if (int e = set_dev(h)) return e;
+  if ((int64_t)h->norms.n < 2 * iters)
+    if (int e = h->norms.alloc(2 * iters)) return e;
+  const bool want_stop = stop != nullptr;
+  if (h->alg == PCB_ALG_AP && want_stop && !h->yprev.p)
+    if (int e = h->yprev.alloc((size_t)h->r * h->n)) return e;
+  for (int64_t k = 0; k < iters; ++k) {
+    double* mon = h->norms.p + k;
+    double* stp = h->norms.p + iters + k;
+    int rc = 0;
+    if (h->alg == PCB_ALG_BCD)
+      rc = bcd_sweep(h, mon, stp);
+    else if (h->alg == PCB_ALG_AP)
+      rc = ap_step(h, mon, stp, want_stop);
+    else
+      rc = fista_step(h, mon, stp);
+    if (rc) return rc;
+  }
+  h->have_shadow = true;
+  h->y_valid = true;
+  h->have_check = false;
+  if (monitor)
+    CUDA_TRY(cudaMemcpyAsync(monitor, h->norms.p, iters * sizeof(double), cudaMemcpyDeviceToHost,
+                             h->stream));
+  if (stop)
+    CUDA_TRY(cudaMemcpyAsync(stop, h->norms.p + iters, iters * sizeof(double),
+                             cudaMemcpyDeviceToHost, h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }

@@ -20,9 +20,11 @@ extra primal thresholds evaluated in the same pass; each check keeps the
 smallest-gap one (ties -> earlier entry), which certifies integer instances
 with exact-zero plateaus; ``level_sets=True`` adds, at
 every check, the best level set of x (best_level_set_gap, certify.py:50-65,
-as one device sort), which is never worse than any threshold.  The algorithms "bcd", "ap" and
-"fista" are accepted by ``SolverConfig`` for compatibility but are outside
-this path and raise NotImplementedError in ``solve``.
+as one device sort), which is never worse than any threshold.
+
+The other dual schemes ("bcd", "ap", "fista") run on the same exact fp64
+kernels (``pcb_dual_init`` / ``pcb_dual_run``) with the reference's loop,
+monitors and dual_tol rules; their iterates are bitwise the reference's.
 """
 from __future__ import annotations
 
@@ -259,14 +261,31 @@ class _Driver:
         ce = self.cfg.check_every
         return min(((k // ce) + 1) * ce, self.kmax)
 
-    def finish(self):
+    def warm_y(self):
+        """Warm-start iterate for the y-based schemes (warm_or("y"), solvers.py:150-165)."""
+        ws = self.cfg.warm_start
+        if ws is None:
+            return None
+        fp = instance_fingerprint(self.g)
+        if ws.fingerprint is not None and ws.fingerprint != fp and not self.cfg.force_warm:
+            raise ValueError("warm start fingerprint does not match instance")
+        for name in ("y", "z"):
+            v = getattr(ws, name, None)
+            if v is not None:
+                if v.shape != self.shape:
+                    raise ValueError("warm start shape %r, expected %r" % (v.shape, self.shape))
+                return np.asarray(v, dtype=np.float64)
+        return None
+
+    def finish(self, state=None):
         wall = time.perf_counter() - self.t0
         lab, x = (self.best_solver or self.solver).get_best()
         certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
         if self.cfg.reference is None:
             for row, packed in zip(self.trace, self._labs):
                 row.jaccard = jaccard_packed(packed, self.best_packed)
-        state = _DeviceDualState(self.solver, self.g)
+        if state is None:
+            state = _DeviceDualState(self.solver, self.g)
         return SolveResult(labeling=lab, tv_solution=x, energy=self.best_energy,
                            gap=self.best_gap, iterations=self.iterations, certified=certified,
                            dual_state=state, trace=self.trace, wall_time=wall,
@@ -325,17 +344,53 @@ def _loop(drv, S, k):
             k = nxt
 
 
-def _not_on_path(name):
-    def run(g, dec, cfg):
-        raise NotImplementedError(
-            "algorithm %r is outside the B200 hot path (only 'aar' runs on the device; "
-            "BCD/AP/FISTA are SURVEY 8(f) rank 2)" % name)
-    return run
+def _solve_dual(g, dec, cfg, alg, monitor_name):
+    """Shared loop of the y-based schemes (solvers.py:219-243, 251-269, 318-341)."""
+    if cfg.precision != "f64":
+        raise ValueError("precision=%r: the fp32-state path is AAR-only" % (cfg.precision,))
+    g = as_grid(g)
+    drv = _Driver(g, dec, cfg)
+    S = drv.solver
+    S.dual_init(alg, drv.warm_y())
+    k = 0
+    stepped = False
+    while True:
+        if drv.due(k) and drv.check(k):
+            break
+        if k >= cfg.max_iters:
+            break
+        if cfg.dual_tol > 0:
+            mon, stop = S.dual_run(1, stop=True)
+            drv.record(monitor_name, mon)
+            k += 1
+            stepped = True
+            if stop[0] <= cfg.dual_tol:
+                drv.check(k)
+                break
+        else:
+            nxt = drv.next_due(k)
+            mon, _ = S.dual_run(nxt - k)
+            drv.record(monitor_name, mon)
+            k = nxt
+            stepped = True
+    lam = S.get_z() if (alg == _native.ALG_AP and stepped) else None
+    state = DualState(y=S.shadow_get(), lam=lam, fingerprint=instance_fingerprint(g))
+    return drv.finish(state)
 
 
-solve_bcd = _not_on_path("bcd")
-solve_ap = _not_on_path("ap")
-solve_fista = _not_on_path("fista")
+def solve_bcd(g, dec, cfg):
+    """Cyclic block projections y_j <- Pi_{K_j}(w - sum_{k != j} y_k) (solvers.py:212-243)."""
+    return _solve_dual(g, dec, cfg, _native.ALG_BCD, "dual_objective")
+
+
+def solve_ap(g, dec, cfg):
+    """Alternating projections between K and L (solvers.py:246-269)."""
+    return _solve_dual(g, dec, cfg, _native.ALG_AP, "ap_distance")
+
+
+def solve_fista(g, dec, cfg):
+    """Accelerated projected gradient on the smooth dual, step 1/r (solvers.py:310-341)."""
+    return _solve_dual(g, dec, cfg, _native.ALG_FISTA, "dual_objective")
 
 _SOLVERS = {"bcd": solve_bcd, "ap": solve_ap, "aar": solve_aar, "fista": solve_fista}
 

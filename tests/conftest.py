@@ -48,3 +48,7 @@ def oracle_lib():
 
 def level_cases():
     return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "levels_*.npz")))
+
+
+def dual_cases():
+    return sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "dual_*.npz")))

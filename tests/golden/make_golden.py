@@ -219,6 +219,7 @@ def main():
     save("kat.npz", **d)
 
     make_levels()
+    make_dual()
 
 
 def make_levels():
@@ -250,7 +251,54 @@ def make_levels():
         save("levels_%s.npz" % name, **d)
 
 
+def make_dual():
+    """BCD / AP / FISTA (solvers.py:212-269, 310-341): fixed iterations,
+    gap-stopped and dual_tol-stopped runs."""
+    global _PC
+    pc = import_reference()
+    _PC = pc
+    sys.path.insert(0, REPO)
+    from paracut_b200.instances import synth_image, energy_from_image
+    r = np.random.default_rng(21)
+    grids = [("r2d4", pc.random_grid((13, 11), "2D-4", r)),
+             ("r2d8", pc.random_grid((9, 12), "2D-8", r)),
+             ("r3d6", pc.random_grid((5, 4, 6), "3D-6", r)),
+             ("deg", pc.random_grid((1, 6), "2D-8", r))]
+    ours = energy_from_image(synth_image((20, 18), 3, 2, 6, seed=5), "2D-4", integer=True)
+    grids.append(("i2d4", pc.GridEnergy(ours.dims, "2D-4", ours.w, ours.dir_weights)))
+    mon = {"bcd": "dual_objective", "ap": "ap_distance", "fista": "dual_objective"}
+    for alg in ("bcd", "ap", "fista"):
+        for name, g in grids:
+            dec = pc.decompose_grid(g)
+            d = grid_arrays(g)
+            ks = (1, 6, 40)
+            for k in ks:
+                res = pc.solve(g, dec, pc.SolverConfig(algorithm=alg, max_iters=k,
+                                                       check_every=k + 1))
+                d["y_%d" % k] = res.dual_state.y
+                if res.dual_state.lam is not None:
+                    d["lam_%d" % k] = res.dual_state.lam
+                d["mon_%d" % k] = np.asarray(res.monitor.get(mon[alg], []), dtype=np.float64)
+                d["gap_%d" % k] = np.array(res.trace[-1].gap)
+            d["ks"] = np.array(ks, dtype=np.int64)
+            res = pc.solve(g, dec, pc.SolverConfig(algorithm=alg, gap_tol=1e-6, max_iters=600,
+                                                   check_every=7))
+            d.update(s_iterations=np.array(res.iterations), s_certified=np.array(res.certified),
+                     s_energy=np.array(res.energy), s_labeling=res.labeling,
+                     s_tv=res.tv_solution, s_y=res.dual_state.y,
+                     s_trace_iter=np.array([t.iteration for t in res.trace]),
+                     s_trace_gap=np.array([t.gap for t in res.trace]),
+                     s_trace_dual=np.array([t.dual_objective for t in res.trace]))
+            res = pc.solve(g, dec, pc.SolverConfig(algorithm=alg, dual_tol=1e-3, max_iters=400,
+                                                   check_every=50))
+            d.update(t_iterations=np.array(res.iterations), t_y=res.dual_state.y,
+                     t_trace_iter=np.array([t.iteration for t in res.trace]))
+            save("dual_%s_%s.npz" % (alg, name), **d)
+
+
 if __name__ == "__main__" and "levels" in sys.argv[1:]:
     make_levels()
+elif __name__ == "__main__" and "dual" in sys.argv[1:]:
+    make_dual()
 elif __name__ == "__main__":
     main()

@@ -121,5 +121,7 @@ def test_config_validation_and_other_algorithms():
     with pytest.raises(ValueError, match=">= 1"):
         pc.SolverConfig(threads=0)
     g = pc.GridEnergy((3, 3), "2D-4", np.zeros(9), [np.ones((3, 2)), np.ones((2, 3))])
-    with pytest.raises(NotImplementedError):
-        pc.solve(g, pc.decompose_grid(g), pc.SolverConfig(algorithm="bcd"))
+    # w = 0: every scheme certifies the empty labeling at k = 0
+    for alg in ("bcd", "ap", "aar", "fista"):
+        res = pc.solve(g, pc.decompose_grid(g), pc.SolverConfig(algorithm=alg))
+        assert res.certified and res.iterations == 0 and res.energy == 0.0
