@@ -78,6 +78,9 @@ int pcb_project_L(const double *w, const int64_t *degree, const uint8_t *support
 int pcb_create(const int64_t *dims, int ndim, int conn, int precision, const double *w,
                const double *const *dir_weights, int device, pcb_solver **out);
 int pcb_destroy(pcb_solver *h);
+/* Device memory of destroyed handles stays mapped in a per-device pool for
+ * the next handle; this returns it to the driver. */
+int pcb_release_memory(int device);
 /* r (number of chain families) and n */
 int pcb_shape(const pcb_solver *h, int *r, int64_t *n);
 /* Use this CUDA stream (cudaStream_t as uintptr) for all later launches. */

@@ -20,6 +20,10 @@
 //   k_reduce_*       deterministic fixed-order final reductions
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -650,30 +654,78 @@ int grid_for(int64_t n, int block, int cap) {
 
 // ----------------------------------------------------------------- device buffers
 
+// Device memory comes from a per-device stream-ordered pool that keeps what
+// it has mapped (release threshold lifted): a handle created after another
+// was destroyed reuses the mapped memory instead of paying cudaFree's unmap
+// and cudaMalloc's remap (measured ~250 ms of create + destroy at 16.7M
+// nodes with plain cudaMalloc/cudaFree).  pcb_release_memory trims it.
+cudaMemPool_t g_pool[64] = {};
+
+cudaMemPool_t device_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pool[dev] = pool;
+  }
+  return g_pool[dev];
+}
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool pooled = false;
   int alloc(size_t count) {
     free();
     if (count == 0) count = 1;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    const size_t bytes = count * sizeof(T);
+    cudaError_t e = cudaErrorMemoryAllocation;
+    if (cudaMemPool_t pool = device_pool()) {
+      // allocated in legacy-stream order, complete before any stream uses it
+      e = cudaMallocFromPoolAsync((void**)&p, bytes, pool, 0);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+      pooled = e == cudaSuccess;
+    }
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();
+      e = cudaMalloc(&p, bytes);
+      pooled = false;
+    }
     if (e != cudaSuccess) {
       (void)cudaGetLastError();
       p = nullptr;
-      return fail(PCB_E_NOMEM, "cudaMalloc(%zu bytes): %s", count * sizeof(T),
-                  cudaGetErrorString(e));
+      return fail(PCB_E_NOMEM, "device allocation (%zu bytes): %s", bytes, cudaGetErrorString(e));
     }
     n = count;
     return 0;
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (pooled) {
+        cudaDeviceSynchronize();  // queued work on any stream may still use p
+        cudaFreeAsync(p, 0);
+      } else {
+        cudaFree(p);
+      }
+    }
     p = nullptr;
     n = 0;
   }
   ~DBuf() { free(); }
 };
+
+#include "hostio.cuh"
 
 }  // namespace
 
@@ -1253,20 +1305,33 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
     return code;
   };
   if ((rc = set_dev(h))) return bail(rc);
+  // PCB_TRACE=1: phase timings of the setup on stderr (diagnostics)
+  static const bool trace = getenv("PCB_TRACE") && getenv("PCB_TRACE")[0] == '1';
+  auto t_last = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!trace) return;
+    cudaDeviceSynchronize();
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pcb_create] %-14s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(t - t_last).count());
+    t_last = t;
+  };
+  phase("set_dev");
   setup_geometry(h);
   if ((rc = h->w.alloc(n))) return bail(rc);
-  cudaError_t e = cudaMemcpy(h->w.p, w, n * sizeof(double), cudaMemcpyHostToDevice);
+  cudaError_t e = hostio::h2d(h->w.p, w, n * sizeof(double), 0);
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "upload w: %s", cudaGetErrorString(e)));
   for (int k = 0; k < h->DG.ndir; ++k) {
     const int64_t cnt = dir_size(h, k);
     if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
     if (cnt > 0) {
       if (!dir_weights[k]) return bail(fail(PCB_E_ARG, "direction %d weights are null", k));
-      e = cudaMemcpy(h->dirw[k].p, dir_weights[k], cnt * sizeof(double), cudaMemcpyHostToDevice);
+      e = hostio::h2d(h->dirw[k].p, dir_weights[k], cnt * sizeof(double), 0);
       if (e != cudaSuccess)
         return bail(fail(PCB_E_CUDA, "upload weights: %s", cudaGetErrorString(e)));
     }
   }
+  phase("upload");
   const int64_t rn = (int64_t)h->r * n;
   if ((rc = h->y.alloc(rn))) return bail(rc);
   e = cudaMemset(h->y.p, 0, rn * sizeof(double));
@@ -1279,8 +1344,11 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
     if ((rc = h->cdrift.alloc(n))) return bail(rc);
     if ((rc = h->X32.alloc(n))) return bail(rc);
     if ((rc = h->G32.alloc(n))) return bail(rc);
+    phase("alloc");
     if ((rc = ensure_wf32(h))) return bail(rc);
+    phase("family weights");
     if ((rc = choose_split(h))) return bail(rc);
+    phase("split");
   }
   if (precision == PCB_F64)  // hull spill for the exact kernels (f32 path: lazily, project_K only)
     if ((rc = ensure_spill(h))) return bail(rc);
@@ -1291,7 +1359,21 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
   if ((rc = h->norms.alloc(1))) return bail(rc);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "setup: %s", cudaGetErrorString(e)));
+  phase("rest");
   *out = h;
+  return 0;
+}
+
+int pcb_release_memory(int device) {
+  if (device < 0 || device >= 64) return fail(PCB_E_ARG, "bad device %d", device);
+  if (!g_pool[device]) return 0;
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  CUDA_TRY(cudaSetDevice(device));
+  CUDA_TRY(cudaDeviceSynchronize());
+  const cudaError_t e = cudaMemPoolTrimTo(g_pool[device], 0);
+  cudaSetDevice(cur);
+  if (e != cudaSuccess) return fail(PCB_E_CUDA, "cudaMemPoolTrimTo: %s", cudaGetErrorString(e));
   return 0;
 }
 
@@ -1344,10 +1426,10 @@ int pcb_set_z(pcb_solver* h, const double* z) {
   if (int e = set_dev(h)) return e;
   const int64_t rn = (int64_t)h->r * h->n;
   if (h->precision == PCB_F64) {
-    CUDA_TRY(cudaMemcpyAsync(h->z.p, z, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(hostio::h2d(h->z.p, z, rn * sizeof(double), h->stream));
   } else {
     if (int e = h->tmp.alloc(rn)) return e;
-    CUDA_TRY(cudaMemcpyAsync(h->tmp.p, z, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(hostio::h2d(h->tmp.p, z, rn * sizeof(double), h->stream));
     k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
         h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, famset(h), h->D);
     LAUNCH_CHECK(h);
@@ -1365,14 +1447,14 @@ int pcb_get_z(pcb_solver* h, double* z) {
   if (int e = set_dev(h)) return e;
   const int64_t rn = (int64_t)h->r * h->n;
   if (h->precision == PCB_F64) {
-    CUDA_TRY(cudaMemcpyAsync(z, h->z.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(z, h->z.p, rn * sizeof(double), h->stream));
   } else {
     if (int e = h->tmp.alloc(rn)) return e;
     k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->p32.p, h->cdrift.p,
                                                                      h->tmp.p, h->n, famset(h),
                                                                      h->D);
     LAUNCH_CHECK(h);
-    CUDA_TRY(cudaMemcpyAsync(z, h->tmp.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(z, h->tmp.p, rn * sizeof(double), h->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
@@ -1404,8 +1486,7 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   h->have_shadow = false;
   h->y_valid = false;
   if (step_norms) {
-    CUDA_TRY(cudaMemcpyAsync(step_norms, h->norms.p, iters * sizeof(double),
-                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(step_norms, h->norms.p, iters * sizeof(double), h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   return 0;
@@ -1426,13 +1507,12 @@ int pcb_shadow(pcb_solver* h, double* y_out, double* s_out) {
   h->y_valid = true;
   const int64_t rn = (int64_t)h->r * h->n;
   if (y_out)
-    CUDA_TRY(cudaMemcpyAsync(y_out, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(y_out, h->y.p, rn * sizeof(double), h->stream));
   if (s_out) {
     k_sum_classes<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->y.p, h->r, h->n,
                                                                         h->xcur.p);
     LAUNCH_CHECK(h);
-    CUDA_TRY(cudaMemcpyAsync(s_out, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
-                             h->stream));
+    CUDA_TRY(hostio::d2h(s_out, h->xcur.p, h->n * sizeof(double), h->stream));
     h->have_check = false;
   }
   if (y_out || s_out) CUDA_TRY(cudaStreamSynchronize(h->stream));
@@ -1444,7 +1524,7 @@ int pcb_shadow_get(pcb_solver* h, double* y_out) {
   if (!h->y_valid) return fail(PCB_E_STATE, "no current shadow");
   if (int e = set_dev(h)) return e;
   const int64_t rn = (int64_t)h->r * h->n;
-  CUDA_TRY(cudaMemcpyAsync(y_out, h->y.p, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(hostio::d2h(y_out, h->y.p, rn * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -1468,7 +1548,7 @@ int pcb_shadow_delta(pcb_solver* h, double* delta) {
     LAUNCH_CHECK(h);
     k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p, 1);
     LAUNCH_CHECK(h);
-    CUDA_TRY(cudaMemcpyAsync(delta, h->norms.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(delta, h->norms.p, sizeof(double), h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   return 0;
@@ -1487,8 +1567,7 @@ int pcb_apply(pcb_solver* h, double* step_norm) {
   }
   h->have_shadow = false;
   if (step_norm) {
-    CUDA_TRY(cudaMemcpyAsync(step_norm, h->norms.p, sizeof(double), cudaMemcpyDeviceToHost,
-                             h->stream));
+    CUDA_TRY(hostio::d2h(step_norm, h->norms.p, sizeof(double), h->stream));
     CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   return 0;
@@ -1501,8 +1580,7 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
   if (!h->have_shadow) return fail(PCB_E_STATE, "check needs a current shadow (call pcb_shadow)");
   if (int e = set_dev(h)) return e;
   // thresholds travel in the tail of vals[]
-  CUDA_TRY(cudaMemcpyAsync(h->vals.p + 48, thr, nthr * sizeof(double), cudaMemcpyHostToDevice,
-                           h->stream));
+  CUDA_TRY(hostio::h2d(h->vals.p + 48, thr, nthr * sizeof(double), h->stream));
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   const int nv = nthr + 3;
   k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n, nthr, h->vals.p + 48,
@@ -1517,7 +1595,7 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
   k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nthr, h->vals.p + 16);
   LAUNCH_CHECK(h);
   double hv[32];
-  CUDA_TRY(cudaMemcpyAsync(hv, h->vals.p, 32 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(hostio::d2h(hv, h->vals.p, 32 * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   const double dual = hv[nthr];
   for (int t = 0; t < nthr; ++t) {
@@ -1543,19 +1621,18 @@ int pcb_get_check(pcb_solver* h, int t, uint8_t* labels, int packed, double* x) 
         if (int e = h->packed.alloc(nb)) return e;
       k_pack<<<grid_for(nb, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t, h->packed.p);
       LAUNCH_CHECK(h);
-      CUDA_TRY(cudaMemcpyAsync(labels, h->packed.p, nb, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(hostio::d2h(labels, h->packed.p, nb, h->stream));
     } else {
       if ((int64_t)h->packed.n < h->n)
         if (int e = h->packed.alloc(h->n)) return e;
       k_labels<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t,
                                                                       h->packed.p);
       LAUNCH_CHECK(h);
-      CUDA_TRY(cudaMemcpyAsync(labels, h->packed.p, h->n, cudaMemcpyDeviceToHost, h->stream));
+      CUDA_TRY(hostio::d2h(labels, h->packed.p, h->n, h->stream));
     }
   }
   if (x)
-    CUDA_TRY(cudaMemcpyAsync(x, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
-                             h->stream));
+    CUDA_TRY(hostio::d2h(x, h->xcur.p, h->n * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -1583,10 +1660,9 @@ int pcb_get_best(pcb_solver* h, uint8_t* labels, double* x) {
   if (!h->have_best) return fail(PCB_E_STATE, "no best iterate kept");
   if (int e = set_dev(h)) return e;
   if (labels)
-    CUDA_TRY(cudaMemcpyAsync(labels, h->bestlab.p, h->n, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(labels, h->bestlab.p, h->n, h->stream));
   if (x)
-    CUDA_TRY(cudaMemcpyAsync(x, h->bestx.p, h->n * sizeof(double), cudaMemcpyDeviceToHost,
-                             h->stream));
+    CUDA_TRY(hostio::d2h(x, h->bestx.p, h->n * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -1599,7 +1675,7 @@ int pcb_dual_init(pcb_solver* h, int alg, const double* y0) {
   if (int e = set_dev(h)) return e;
   const int64_t rn = (int64_t)h->r * h->n;
   if (y0)
-    CUDA_TRY(cudaMemcpyAsync(h->y.p, y0, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    CUDA_TRY(hostio::h2d(h->y.p, y0, rn * sizeof(double), h->stream));
   else
     CUDA_TRY(cudaMemsetAsync(h->y.p, 0, rn * sizeof(double), h->stream));
   if (alg == PCB_ALG_FISTA)  // v = y.copy()
@@ -1645,11 +1721,9 @@ int pcb_dual_run(pcb_solver* h, int64_t iters, double* monitor, double* stop) {
   h->y_valid = true;
   h->have_check = false;
   if (monitor)
-    CUDA_TRY(cudaMemcpyAsync(monitor, h->norms.p, iters * sizeof(double), cudaMemcpyDeviceToHost,
-                             h->stream));
+    CUDA_TRY(hostio::d2h(monitor, h->norms.p, iters * sizeof(double), h->stream));
   if (stop)
-    CUDA_TRY(cudaMemcpyAsync(stop, h->norms.p + iters, iters * sizeof(double),
-                             cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(hostio::d2h(stop, h->norms.p + iters, iters * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -1671,7 +1745,7 @@ int pcb_level_set(pcb_solver* h, const double* x, double* u, double* energy) {
   const double* xd = h->xcur.p;
   if (x) {
     if (int e = xin.alloc(n)) return e;
-    CUDA_TRY(cudaMemcpyAsync(xin.p, x, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(hostio::h2d(xin.p, x, n * sizeof(double), st));
     xd = xin.p;
   }
   if (int e = xs.alloc(n)) return e;
@@ -1696,7 +1770,7 @@ int pcb_level_set(pcb_solver* h, const double* x, double* u, double* energy) {
   CUDA_TRY(cub::DeviceScan::InclusiveSum(tmp.p, bytes, flag.p, rs.p, ni, st));
   flag.free();
   int K = 0;
-  CUDA_TRY(cudaMemcpyAsync(&K, rs.p + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(hostio::d2h(&K, rs.p + (n - 1), sizeof(int), st));
   CUDA_TRY(cudaStreamSynchronize(st));
   if (int e = rank_of.alloc(n)) return e;
   if (int e = ws.alloc(n)) return e;
@@ -1728,7 +1802,7 @@ int pcb_level_set(pcb_solver* h, const double* x, double* u, double* energy) {
   L::k_argmin_final<<<1, 1, 0, st>>>(parts.p, ga, xs.p, last_of.p, out.p);
   LAUNCH_CHECK(h);
   double hv[3];
-  CUDA_TRY(cudaMemcpyAsync(hv, out.p, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(hostio::d2h(hv, out.p, sizeof(hv), st));
   CUDA_TRY(cudaStreamSynchronize(st));
   *u = hv[0];
   if (energy) *energy = hv[1];
@@ -1745,10 +1819,10 @@ int pcb_project_K(pcb_solver* h, const double* v, double* out) {
     if (int e = h->tmp.alloc(2 * rn)) return e;
   double* src = h->tmp.p;
   double* dst = h->tmp.p + rn;
-  CUDA_TRY(cudaMemcpyAsync(src, v, rn * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(hostio::h2d(src, v, rn * sizeof(double), h->stream));
   CUDA_TRY(cudaMemsetAsync(dst, 0, rn * sizeof(double), h->stream));
   if (int e = sweep_exact(h, src, dst)) return e;
-  CUDA_TRY(cudaMemcpyAsync(out, dst, rn * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(hostio::d2h(out, dst, rn * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -1835,18 +1909,18 @@ int pcb_project_L(const double* w, const int64_t* degree, const uint8_t* support
   if (int e = d_deg.alloc(n)) return e;
   if (int e = d_sup.alloc(rn)) return e;
   if (int e = d_bad.alloc(1)) return e;
-  CUDA_TRY(cudaMemcpy(d_w.p, w, n * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_v.p, v, rn * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_deg.p, degree, n * sizeof(int64_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_sup.p, support, rn, cudaMemcpyHostToDevice));
+  CUDA_TRY(hostio::h2d(d_w.p, w, n * sizeof(double), 0));
+  CUDA_TRY(hostio::h2d(d_v.p, v, rn * sizeof(double), 0));
+  CUDA_TRY(hostio::h2d(d_deg.p, degree, n * sizeof(int64_t), 0));
+  CUDA_TRY(hostio::h2d(d_sup.p, support, rn, 0));
   CUDA_TRY(cudaMemset(d_bad.p, 0, sizeof(int)));
   k_project_L<<<grid_for(n, 256, NODE_GRID), 256>>>(d_w.p, d_deg.p, d_sup.p, r, n, d_v.p, d_out.p,
                                                     d_bad.p);
   LAUNCH_CHECK((pcb_solver*)nullptr);
   int bad = 0;
-  CUDA_TRY(cudaMemcpy(&bad, d_bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(hostio::d2h(&bad, d_bad.p, sizeof(int), 0));
   if (bad) return fail(PCB_E_ARG, "w has mass on coordinates covered by no class");
-  CUDA_TRY(cudaMemcpy(out, d_out.p, rn * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(hostio::d2h(out, d_out.p, rn * sizeof(double), 0));
   return 0;
 }
 
@@ -1861,7 +1935,7 @@ static int csr_spill(int64_t nch, const int64_t* lens_host, DBuf<int64_t>& soff,
   }
   if (tot == 0) tot = 1;
   if (int e = soff.alloc(off.size())) return e;
-  CUDA_TRY(cudaMemcpy(soff.p, off.data(), off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(hostio::h2d(soff.p, off.data(), off.size() * sizeof(int64_t), 0));
   if (int e = cx.alloc(tot)) return e;
   if (int e = fx.alloc(tot)) return e;
   if (int e = cy.alloc(tot)) return e;
@@ -1892,20 +1966,20 @@ int pcb_prox_chains(const int64_t* node_idx, const int64_t* chain_ptr, const dou
   if (int e = d_ew.alloc(n_edges)) return e;
   if (int e = d_v.alloc(n_nodes)) return e;
   if (int e = d_out.alloc(n_nodes)) return e;
-  CUDA_TRY(cudaMemcpy(d_idx.p, node_idx, n_idx * sizeof(int64_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_ptr.p, chain_ptr, (c_hi + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(hostio::h2d(d_idx.p, node_idx, n_idx * sizeof(int64_t), 0));
+  CUDA_TRY(hostio::h2d(d_ptr.p, chain_ptr, (c_hi + 1) * sizeof(int64_t), 0));
   if (n_edges > 0 && edge_w)
-    CUDA_TRY(cudaMemcpy(d_ew.p, edge_w, n_edges * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_v.p, v, n_nodes * sizeof(double), cudaMemcpyHostToDevice));
+    CUDA_TRY(hostio::h2d(d_ew.p, edge_w, n_edges * sizeof(double), 0));
+  CUDA_TRY(hostio::h2d(d_v.p, v, n_nodes * sizeof(double), 0));
   // out is updated only on chain nodes: start from the caller's contents
-  CUDA_TRY(cudaMemcpy(d_out.p, out, n_nodes * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(hostio::h2d(d_out.p, out, n_nodes * sizeof(double), 0));
   if (int e = csr_spill(nch, lens.data(), soff, cx, cy, fx, fy)) return e;
   Spill sp{cx.p, cy.p, fx.p, fy.p};
   const int g = (int)((nch + FAM_BLOCK - 1) / FAM_BLOCK);
   k_prox_csr<<<g, FAM_BLOCK>>>(d_idx.p, d_ptr.p, d_ew.p, c_lo, c_hi, d_v.p, d_out.p,
                                as_projection ? 1 : 0, sp, soff.p);
   LAUNCH_CHECK((pcb_solver*)nullptr);
-  CUDA_TRY(cudaMemcpy(out, d_out.p, n_nodes * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(hostio::d2h(out, d_out.p, n_nodes * sizeof(double), 0));
   return 0;
 }
 
@@ -1928,15 +2002,15 @@ int pcb_tv1d_prox_batch(const double* s, const double* a, const int64_t* ptr, in
   if (int e = d_s.alloc(total)) return e;
   if (int e = d_a.alloc(nedge)) return e;
   if (int e = d_x.alloc(total)) return e;
-  CUDA_TRY(cudaMemcpy(d_ptr.p, ptr, (nchains + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(d_s.p, s, total * sizeof(double), cudaMemcpyHostToDevice));
-  if (nedge > 0 && a) CUDA_TRY(cudaMemcpy(d_a.p, a, nedge * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(hostio::h2d(d_ptr.p, ptr, (nchains + 1) * sizeof(int64_t), 0));
+  CUDA_TRY(hostio::h2d(d_s.p, s, total * sizeof(double), 0));
+  if (nedge > 0 && a) CUDA_TRY(hostio::h2d(d_a.p, a, nedge * sizeof(double), 0));
   if (int e = csr_spill(nchains, lens.data(), soff, cx, cy, fx, fy)) return e;
   Spill sp{cx.p, cy.p, fx.p, fy.p};
   const int g = (int)((nchains + FAM_BLOCK - 1) / FAM_BLOCK);
   k_tv1d<<<g, FAM_BLOCK>>>(d_s.p, d_a.p, d_ptr.p, nchains, d_x.p, sp, soff.p);
   LAUNCH_CHECK((pcb_solver*)nullptr);
-  CUDA_TRY(cudaMemcpy(x, d_x.p, total * sizeof(double), cudaMemcpyDeviceToHost));
+  CUDA_TRY(hostio::d2h(x, d_x.p, total * sizeof(double), 0));
   return 0;
 }
 
