@@ -81,6 +81,9 @@ int pcb_destroy(pcb_solver *h);
 /* Device memory of destroyed handles stays mapped in a per-device pool for
  * the next handle; this returns it to the driver. */
 int pcb_release_memory(int device);
+/* Diagnostics: sweep counters (warp trips, lane gates, bends, tiles issued,
+ * tiles retired) of a build compiled with -DPCB_COUNT; zeros otherwise. */
+int pcb_debug_counters(uint64_t *out, int reset);
 /* r (number of chain families) and n */
 int pcb_shape(const pcb_solver *h, int *r, int64_t *n);
 /* Use this CUDA stream (cudaStream_t as uintptr) for all later launches. */

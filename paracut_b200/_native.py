@@ -66,6 +66,7 @@ def _declare(L):
     L.pcb_level_set.argtypes = [P, P, P, P]
     L.pcb_dual_init.argtypes = [P, INT, P]
     L.pcb_release_memory.argtypes = [INT]
+    L.pcb_debug_counters.argtypes = [P, INT]
     L.pcb_dual_run.argtypes = [P, I64, P, P]
     L.pcb_project_K.argtypes = [P, P, P]
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
@@ -82,7 +83,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
-           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
 
 
@@ -126,6 +127,13 @@ def device_count():
 def release_memory(device=0):
     """Return the device memory destroyed handles left in the reuse pool."""
     check(lib().pcb_release_memory(int(device)))
+
+
+def debug_counters(reset=True):
+    """Sweep counters of a -DPCB_COUNT build (zeros in the normal build)."""
+    out = np.zeros(8, dtype=np.uint64)
+    check(lib().pcb_debug_counters(ptr(out), int(bool(reset))))
+    return out
 
 
 def _f64(a):

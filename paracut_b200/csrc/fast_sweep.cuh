@@ -36,6 +36,14 @@
 namespace pcb {
 namespace fast {
 
+#ifdef PCB_COUNT
+// diagnostics build only: warp trips, lane gates, bends, tiles issued, tiles retired
+__device__ unsigned long long g_count[8];
+#define PCB_CNT(i, v) (lane == 0 ? atomicAdd(&g_count[i], (unsigned long long)(v)) : 0ull)
+#else
+#define PCB_CNT(i, v) 0ull
+#endif
+
 constexpr int TP = 8;          // positions per tile
 constexpr int NT = 4;          // tiles in the ring
 constexpr int RL = TP * NT;    // ring length (positions)
@@ -178,8 +186,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   const bool valid = lane < nvalid;
   const int64_t c = c0 + lane;
   const int m = F.m;
-  const int64_t my_base = valid ? fam_base(F, c) : 0;
   const int64_t C = F.C;
+  // 32-bit index arithmetic: pcb_create keeps n below 2^31, so every node
+  // index and interleaved index pos * C + c fits (half the address IMADs)
+  const int C32 = (int)F.C, c32 = (int)c;
+  const int ns32 = (int)F.ns, zz32 = (int)F.zz, ph32 = F.phase;
+  const int base32 = valid ? (int)fam_base(F, c) : 0;
+  auto node = [&](int b, int pos) { return b + pos * ns32 + zz32 * ((pos + ph32) & 1); };
+  // mode B (row-like families): lane works on chains 8*(lane/8) + ib, ib < 8;
+  // their node bases are fixed for the whole launch
+  int bB[8];
+  if (ROWLIKE) {
+#pragma unroll
+    for (int ib = 0; ib < 8; ++ib) bB[ib] = __shfl_sync(0xffffffffu, base32, ((lane >> 3) << 3) + ib);
+  }
 
   // this unit's range [start, stop) of the chain and the tube touches there;
   // the string is forced through the next unit's merge point at gate `stop`
@@ -234,22 +254,23 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 
   int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
   if (has && start > 0 && stouch != 0)  // anchored on a tube touch: skr = -touch * a(start-1)
-    skr = (R)(-(double)stouch * (double)A.wf[(int64_t)(start - 1) * C + c]);
+    skr = (R)(-(double)stouch * (double)A.wf[((start - 1) * C32 + c32)]);
   // end value offset at `stop`: the string ends at S_stop + touch * a(stop-1)
   const R eoff = (has && stop < m && etouch != 0)
-                     ? (R)((double)etouch * (double)A.wf[(int64_t)(stop - 1) * C + c]) : R(0);
+                     ? (R)((double)etouch * (double)A.wf[((stop - 1) * C32 + c32)]) : R(0);
 
   auto issue = [&](int T) {
     const int k0 = T * TP;
+    PCB_CNT(3, 1);
 #pragma unroll
     for (int q = 0; q < TP; ++q) {  // mode A
       const int pos = k0 + q;
       const bool pr = valid && pos < m;
-      const int64_t fi = pr ? (int64_t)pos * C + c : 0;
+      const int fi = pr ? (pos * C32 + c32) : 0;
       cp4(&rp[rix(lane, pos)], A.p + fi, pr);
       cp4(&ra[rix(lane, pos)], A.wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
       if (!ROWLIKE) {
-        const int64_t nd = pr ? fam_node(F, my_base, pos) : 0;
+        const int nd = pr ? node(base32, pos) : 0;
         cp8(&rz[rix(lane, pos)], A.c + nd, pr);
       }
     }
@@ -259,9 +280,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
-        const int64_t bi = __shfl_sync(0xffffffffu, my_base, i);
+        const int bi = bB[ib];
         const bool pr = i < nvalid && pos < m;
-        const int64_t nd = pr ? fam_node(F, bi, pos) : 0;
+        const int nd = pr ? node(bi, pos) : 0;
         cp8(&rz[rix(i, pos)], A.c + nd, pr);
       }
     }
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       for (int q = 0; q < TP; ++q) {
         const int pos = k0 + q;
         const bool pr = valid && pos < m;
-        const int64_t nd = pr ? fam_node(F, my_base, pos) : 0;
+        const int nd = pr ? node(base32, pos) : 0;
         gpre[q] = pr ? A.G[nd] : 0.f;
         if (ROLE == LAST) xpre[q] = pr ? A.X[nd] : 0.f;
       }
@@ -287,9 +308,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
-        const int64_t bi = __shfl_sync(0xffffffffu, my_base, i);
+        const int bi = bB[ib];
         const bool pr = i < nvalid && pos < m;
-        const int64_t nd = pr ? fam_node(F, bi, pos) : 0;
+        const int nd = pr ? node(bi, pos) : 0;
         gpre[ib] = pr ? A.G[nd] : 0.f;
         if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : 0.f;
       }
@@ -307,6 +328,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 
   // lockstep retire of tile T: per-node outputs from (z, segment markers), write back
   auto retire = [&](int T) {
+    PCB_CNT(4, 1);
     if (pre_tile != T) prefetch(T);
     const int k0 = T * TP;
 #pragma unroll
@@ -322,16 +344,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         }
         const double pn = (zj - zs) + qs;
         if (ROLE == SHADOW) {
-          if (!ROWLIKE) A.y[fam_node(F, my_base, pos)] = pn;
+          if (!ROWLIKE) A.y[node(base32, pos)] = pn;
           else rz[ix] = pn;
         } else {
           const float pold = rp[ix];
           const float p32 = (float)pn;
           const double d = (double)p32 - (double)pold;
           nrm += d * d;
-          A.p[(int64_t)pos * C + c] = p32;
+          A.p[(pos * C32 + c32)] = p32;
           if (!ROWLIKE) {
-            const int64_t nd = fam_node(F, my_base, pos);
+            const int nd = node(base32, pos);
             if (ROLE == FIRST) {
               A.G[nd] = (float)d;
             } else if (ROLE == MID) {
@@ -354,19 +376,20 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     }
     smask &= ~(0xffu << ((k0 & (RL - 1))));
     if (ROWLIKE) {
+      // positions of this tile my chain emitted: [max(start, k0), min(stop, i0))
+      const int lo = max(start, k0) - k0, hi = min(min(stop, i0), k0 + TP) - k0;
+      const unsigned emask = (has && hi > lo) ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
       __syncwarp();
-      const int pos = k0 + (lane & 7);
+      const int q = lane & 7;
+      const int pos = k0 + q;
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
-        const int i0_i = __shfl_sync(0xffffffffu, i0, i);
-        const int st_i = __shfl_sync(0xffffffffu, start, i);
-        const int sp_i = __shfl_sync(0xffffffffu, stop, i);
-        const bool has_i = __shfl_sync(0xffffffffu, has, i);
-        const int64_t bi = __shfl_sync(0xffffffffu, my_base, i);
-        if (has_i && pos >= st_i && pos < sp_i && pos < i0_i) {
+        const unsigned em_i = __shfl_sync(0xffffffffu, emask, i);
+        const int bi = bB[ib];
+        if ((em_i >> q) & 1u) {
           const int ix = rix(i, pos);
-          const int64_t nd = fam_node(F, bi, pos);
+          const int nd = node(bi, pos);
           if (ROLE == SHADOW) {
             A.y[nd] = rz[ix];
           } else if (ROLE == FIRST) {
@@ -400,14 +423,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     float an = ra[rix(lane, k)];
     for (;;) {
       const bool act = !done && k < avail_hi;
-      if (__popc(__ballot_sync(0xffffffffu, act)) <= keep_min) break;
+      const int nact = __popc(__ballot_sync(0xffffffffu, act));
+      if (nact <= keep_min) break;
+      PCB_CNT(0, 1);
+      PCB_CNT(1, nact);
       if (act) {
         const int kp = k;
         double zabs = zn;
         float af = an;
         if (LAG && kp < lo_pos) {  // lagging lane below the ring
-          const int64_t fi = (int64_t)kp * C + c;
-          zabs = z_global(A, fi, fam_node(F, my_base, kp));
+          const int fi = (kp * C32 + c32);
+          zabs = z_global(A, fi, node(base32, kp));
           af = kp < m - 1 ? (float)a_global(A, fi) : 0.f;
         }
         k = kp + 1;
@@ -440,6 +466,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         const bool ec = e && c0x != pe && Lc < sE;
         const bool ef = e && !ec && f0x != pe && Lf > sE;
         const bool bend = b1 || b2 || e;
+#ifdef PCB_COUNT
+        if (bend) atomicAdd(&g_count[2], 1ull);
+#endif
         const bool tf = b1 || ef;  // touches the floor
         const bool tc = b2 || ec;  // touches the ceiling
         const int bk = tf ? f0x : (tc ? c0x : pe);
@@ -450,10 +479,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         R qv = -fill;  // q = z_i0 - fill, and z_i0 - t = 0
         if (LAG && bend && i0 < lo_pos) {
           const double fabs_ = (double)fill + t;
-          if (bk - 1 < lo_pos) ab = (R)a_global(A, (int64_t)(bk - 1) * C + c);
+          if (bk - 1 < lo_pos) ab = (R)a_global(A, ((bk - 1) * C32 + c32));
           const int e2 = min(min(bk, lo_pos), stop);
           for (int j = i0; j < e2; ++j)
-            nrm += finish_global<ROLE>(A, (int64_t)j * C + c, fam_node(F, my_base, j), fabs_);
+            nrm += finish_global<ROLE>(A, (j * C32 + c32), node(base32, j), fabs_);
           s0 = e2;
           if (s0 < bk) qv = (R)((rz[rix(lane, s0)] - t) - (double)fill);
         }
@@ -649,7 +678,10 @@ __global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, co
   const int nvalid = (int)min((int64_t)32, C - c0);
   const bool valid = lane < nvalid;
   const int64_t c = c0 + lane;
-  const int64_t base = valid ? fam_base(F, c) : 0;
+  const int C32 = (int)C, c32 = (int)c;  // n < 2^31: 32-bit index math
+  const int ns32 = (int)F.ns, zz32 = (int)F.zz, ph32 = F.phase;
+  const int base = valid ? (int)fam_base(F, c) : 0;
+  auto node = [&](int bb, int pos) { return bb + pos * ns32 + zz32 * ((pos + ph32) & 1); };
   double* z_s = sz[wib];
   float* a_s = sa[wib];
   float* p_s = sp[wib];
@@ -658,20 +690,20 @@ __global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, co
   for (int q = 0; q < MW; ++q) {
     const int pos = g + q;
     const bool pr = valid && pos < m;
-    const int64_t fi = pr ? (int64_t)pos * C + c : 0;
+    const int fi = pr ? pos * C32 + c32 : 0;
     cp4(&p_s[mix(lane, q)], p + fi, pr);
     cp4(&a_s[mix(lane, q)], wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
-    if (!ROWLIKE) cp8(&z_s[mix(lane, q)], cdr + (pr ? fam_node(F, base, pos) : 0), pr);
+    if (!ROWLIKE) cp8(&z_s[mix(lane, q)], cdr + (pr ? node(base, pos) : 0), pr);
   }
   if (ROWLIKE) {
 #pragma unroll 4
     for (int ib = 0; ib < 32; ib += 32 / MW) {
       const int i = ib + lane / MW;
       const int q = lane % MW;
-      const int64_t bi = __shfl_sync(0xffffffffu, base, i);
+      const int bi = __shfl_sync(0xffffffffu, base, i);
       const int pos = g + q;
       const bool pr = i < nvalid && pos < m;
-      cp8(&z_s[mix(i, q)], cdr + (pr ? fam_node(F, bi, pos) : 0), pr);
+      cp8(&z_s[mix(i, q)], cdr + (pr ? node(bi, pos) : 0), pr);
     }
   }
   cp_commit();
@@ -691,13 +723,13 @@ __global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, co
       *z = z_s[ix];
       *a = (double)a_s[ix];
     } else {
-      const int64_t fi = (int64_t)pos * C + c;
-      *z = (double)__ldg(p + fi) + __ldg(cdr + fam_node(F, base, pos));
+      const int fi = pos * C32 + c32;
+      *z = (double)__ldg(p + fi) + __ldg(cdr + node(base, pos));
       *a = pos < m - 1 ? (double)__ldg(wf + fi) : 0.0;
     }
   };
   int out = -1;
-  const double ag = (double)__ldg(wf + (int64_t)(g - 1) * C + c);
+  const double ag = (double)__ldg(wf + (g - 1) * C32 + c32);
   if (ag == 0.0) {
     out = g * 4 + 1;  // zero-weight gate: a piece starts here for every string
   } else {

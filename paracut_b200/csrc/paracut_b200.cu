@@ -1364,6 +1364,24 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
   return 0;
 }
 
+int pcb_debug_counters(uint64_t* out, int reset) {
+  if (!out) return fail(PCB_E_ARG, "null argument");
+#ifdef PCB_COUNT
+  unsigned long long v[8];
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(v, pcb::fast::g_count, sizeof(v)));
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  if (reset) {
+    unsigned long long z[8] = {};
+    CUDA_TRY(cudaMemcpyToSymbol(pcb::fast::g_count, z, sizeof(z)));
+  }
+#else
+  (void)reset;
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+#endif
+  return 0;
+}
+
 int pcb_release_memory(int device) {
   if (device < 0 || device >= 64) return fail(PCB_E_ARG, "bad device %d", device);
   if (!g_pool[device]) return 0;
