@@ -39,9 +39,9 @@ namespace fast {
 #ifdef PCB_COUNT
 // diagnostics build only: warp trips, lane gates, bends, tiles issued, tiles retired
 __device__ unsigned long long g_count[8];
-#define PCB_CNT(i, v) (lane == 0 ? atomicAdd(&g_count[i], (unsigned long long)(v)) : 0ull)
+#define PCB_CNT(i, v) ((void)(lane == 0 ? atomicAdd(&g_count[i], (unsigned long long)(v)) : 0ull))
 #else
-#define PCB_CNT(i, v) 0ull
+#define PCB_CNT(i, v) ((void)0)
 #endif
 
 constexpr int TP = 8;          // positions per tile
@@ -79,15 +79,22 @@ struct Args {
   int export_g;     // LAST: also store the per-node g = sum_j d_j (fp32) in G
 };
 
+// Predicated copies (no zero fill): slots of positions past the chain end or
+// of lanes without a chain are never read, so skipping them is enough and
+// avoids the src-size arithmetic of the zero-filling form.
 __device__ __forceinline__ void cp4(void* dst, const void* src, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = pred ? 4 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(src), "r"(n));
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%1], 4;\n}\n" ::"r"(s),
+      "l"(src), "r"((int)pred));
 }
 __device__ __forceinline__ void cp8(void* dst, const void* src, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src), "r"(n));
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n"
+      " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(s),
+      "l"(src), "r"((int)pred));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait(int pending) {
