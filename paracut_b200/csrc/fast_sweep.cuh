@@ -128,8 +128,10 @@ __device__ __forceinline__ double rcp_r<double>(int di) {
   return rcp_small(di, (double)di);
 }
 
-// ring index of (lane row l, position pos)
-__device__ __forceinline__ int rix(int l, int pos) { return (l << 5) | ((pos & (RL - 1)) ^ l); }
+// ring index of (lane row l, position pos): (l << 5) | ((pos & 31) ^ l), written
+// as one masked XOR with (l << 5 | l) so it is a single LOP3 (the scan is
+// ALU-pipe bound)
+__device__ __forceinline__ int rix(int l, int pos) { return (pos & (RL - 1)) ^ ((l << 5) | l); }
 
 template <int ROLE>
 __host__ __device__ constexpr int ring_bytes_host() {
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       start = stop = 0;
     }
   }
+  if (!has) start = stop = 0;  // lanes without a unit (past the last chain) are finished
   const int rlo = __reduce_min_sync(0xffffffffu, has ? start : 0x7fffffff);
   const int rhi = __reduce_max_sync(0xffffffffu, has ? stop : 0);
   const int t_first = rlo == 0x7fffffff ? 0 : rlo / TP;
@@ -245,13 +248,15 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   // anchor's z, so they stay O(|p| + local drift) and fp32 keeps ~1e-7 of
   // them) and in fp64 for the shadow, whose output feeds the certificates.
   using R = typename std::conditional<ROLE == SHADOW, double, float>::type;
-  int i0 = start, pe = m, k = start, c0x = -1, f0x = -1;
+  // a lane is finished when its anchor reaches `stop` (lanes without a unit
+  // have start = stop = 0); it is never active again, and its whole range
+  // counts as emitted
+  int i0 = start, k = start, c0x = -1, f0x = -1;
   double t = 0.0;          // z at the anchor: scan values are z - t
   bool fresh = true;       // t is taken from the first gate after a (re)start
   R skr = R(0);            // running sum of (z - t) minus the anchor value
   R cs = R(0), Lc = R(0);  // min slope to the ceiling points; cs * (k - i0)
   R fs = R(0), Lf = R(0);  // max slope to the floor points;   fs * (k - i0)
-  bool done = !has;
   unsigned smask = 0u;        // segment starts inside the ring (bit = slot)
   double zs = 0.0, qs = 0.0;  // retire carry: z at the current segment start, q there
 
@@ -428,8 +433,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     // end of the previous trip (slots >= k are never written by the scan)
     double zn = rz[rix(lane, k)];
     float an = ra[rix(lane, k)];
+    const int lim = min(avail_hi, stop);  // gates are consumed while k < lim
+    if (!LAG && fresh && k < lim) {  // first gate of the unit or after a lagging round
+      t = zn;
+      fresh = false;
+    }
     for (;;) {
-      const bool act = !done && k < avail_hi;
+      const bool act = k < lim;
       const int nact = __popc(__ballot_sync(0xffffffffu, act));
       if (nact <= keep_min) break;
       PCB_CNT(0, 1);
@@ -444,13 +454,18 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
           af = kp < m - 1 ? (float)a_global(A, fi) : 0.f;
         }
         k = kp + 1;
-        t = fresh ? zabs : t;
-        fresh = false;
+        if (LAG) {
+          t = fresh ? zabs : t;
+          fresh = false;
+        }
         skr += (R)(zabs - t);
         const bool at_stop = k == stop;  // forced end point (merge point or chain end)
-        const bool inner = k < m && !at_stop;
+        const bool inner = k < stop;     // (stop <= m)
         const R rk = inner ? (R)af : R(0);
-        pe = ((inner && af == 0.f) || at_stop) ? k : pe;
+        // a zero weight (or the unit end) makes this gate a mandatory piece end;
+        // after an earlier bend the rescan reaches the same gate again, so no
+        // piece-end state needs to be kept
+        const bool zw = !inner || af == 0.f;
         const R inv = rcp_r<R>(k - i0);
         Lc += cs;
         Lf += fs;
@@ -469,16 +484,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         fs = fu ? l * inv : fs;
         Lf = fu ? l : Lf;
         const bool b2 = !b1 && fs > cs;       // floor rises over the ceiling cone
-        const bool e = !b1 && !b2 && k == pe;  // piece end: S_pe is mandatory
-        const bool ec = e && c0x != pe && Lc < sE;
-        const bool ef = e && !ec && f0x != pe && Lf > sE;
+        const bool e = !b1 && !b2 && zw;  // piece end: S_k is mandatory
+        const bool ec = e && c0x != k && Lc < sE;
+        const bool ef = e && !ec && f0x != k && Lf > sE;
         const bool bend = b1 || b2 || e;
 #ifdef PCB_COUNT
         if (bend) atomicAdd(&g_count[2], 1ull);
 #endif
         const bool tf = b1 || ef;  // touches the floor
         const bool tc = b2 || ec;  // touches the ceiling
-        const int bk = tf ? f0x : (tc ? c0x : pe);
+        const int bk = tf ? f0x : (tc ? c0x : k);
         const R fill = tf ? fs : (tc ? cs : sE * inv);
         // ---- close segment [i0, bk): its prox value is the string slope `fill` (+ t)
         R ab = (R)ra[rix(lane, bk - 1)];
@@ -500,23 +515,25 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
           else ra[ixs] = (float)qv;
         }
         smask |= mark ? (1u << (s0 & (RL - 1))) : 0u;
-        const bool piece_end = bk == pe;
-        const R nskr = piece_end ? R(0) : (tf ? ab : (tc ? -ab : R(0)));
+        // after a touch the string leaves the tube point: skr = -touch * a(bk-1)
+        // (a free piece end restarts at 0)
+        const R nskr = tf ? ab : (tc ? -ab : R(0));
         i0 = bend ? bk : i0;
         k = bend ? bk : k;
-        fresh = bend;
+        if (LAG) fresh = bend;
         skr = bend ? nskr : skr;
-        pe = (bend && piece_end) ? m : pe;
-        done = bend && bk >= stop;
+        // c0x / f0x = -1 make the next gate overwrite cs, Lc, fs, Lf
         c0x = bend ? -1 : c0x;
         f0x = bend ? -1 : f0x;
-        cs = bend ? R(0) : cs;
-        fs = bend ? R(0) : fs;
-        Lc = bend ? R(0) : Lc;
-        Lf = bend ? R(0) : Lf;
         const int ixn = rix(lane, k);
         zn = rz[ixn];
         an = ra[ixn];
+        // non-lagging: the anchor value of a restarted string is the next gate's
+        // z, unless that gate is not loaded yet (then the next round takes it)
+        if (!LAG) {
+          t = bend ? zn : t;
+          fresh = bend && k >= lim;
+        }
       }
     }
   };
@@ -536,21 +553,21 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       // a variant without any below-the-ring checks, with the segment close
       // fully predicated so the warp stays converged through bends.
       const int keep = (t_rdy < t_ld) ? PCB_SCAN_KEEP : 0;
-      if (__any_sync(0xffffffffu, !done && i0 < lo_pos))
+      if (__any_sync(0xffffffffu, i0 < lo_pos && i0 < stop))
         scan(lo_pos, avail_hi, keep, std::true_type());
       else
         scan(lo_pos, avail_hi, keep, std::false_type());
       __syncwarp();
-      if (__all_sync(0xffffffffu, done)) {
+      if (__all_sync(0xffffffffu, i0 >= stop)) {
         cp_wait(0);
         __syncwarp();
         for (int T = t_lo; T < t_ld; ++T) retire(T);
         break;
       }
       // ---------------- retire tiles every lane has emitted
-      const int front = __reduce_min_sync(0xffffffffu, done ? 0x7fffffff : i0);
+      const int front = __reduce_min_sync(0xffffffffu, i0 < stop ? i0 : 0x7fffffff);
       while (t_lo < t_rdy && (t_lo + 1) * TP <= front) retire(t_lo++);
-      const bool any_act = __any_sync(0xffffffffu, !done && k < avail_hi);
+      const bool any_act = __any_sync(0xffffffffu, k < min(avail_hi, stop));
       if (!any_act && t_rdy == t_ld && t_ld - t_lo == NT)
         retire(t_lo++);  // ring full: lagging lanes go global
       __syncwarp();
