@@ -429,6 +429,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   // (they continue next round), so a few slow lanes do not idle the warp
   auto scan = [&](int lo_pos, int avail_hi, int keep_min, auto lag_tag) {
     constexpr bool LAG = decltype(lag_tag)::value;
+    asm volatile("" : "+r"(keep_min));  // keep it in a register, not re-derived per trip
     // software-pipelined ring reads: the next gate's z and a are loaded at the
     // end of the previous trip (slots >= k are never written by the scan)
     double zn = rz[rix(lane, k)];
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
           if (ROLE == SHADOW) rf[ixs] = (double)qv;
           else ra[ixs] = (float)qv;
         }
-        smask |= mark ? (1u << (s0 & (RL - 1))) : 0u;
+        smask |= (unsigned)mark << (s0 & (RL - 1));
         // after a touch the string leaves the tube point: skr = -touch * a(bk-1)
         // (a free piece end restarts at 0)
         const R nskr = tf ? ab : (tc ? -ab : R(0));
