@@ -533,7 +533,27 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         // z, unless that gate is not loaded yet (then the next round takes it)
         if (!LAG) {
           t = bend ? zn : t;
-          fresh = bend && k >= lim;
+          // The first gate after a restart cannot bend (one point: both cones
+          // coincide, slopes skr +- a over a distance of 1), so it is taken
+          // here instead of in a trip of its own -- about one trip per segment,
+          // i.e. nearly every rescan.  Not at a zero weight or the unit end
+          // (a mandatory piece end) or when position k is not loaded yet.
+          const int k1 = k + 1;
+          const bool triv = bend && k < lim && k1 < stop && an != 0.f;
+          if (triv) {
+            const R rk1 = (R)an;
+            c0x = k1;
+            f0x = k1;
+            cs = skr + rk1;
+            Lc = cs;
+            fs = skr - rk1;
+            Lf = fs;
+            k = k1;
+            const int ix1 = rix(lane, k1);
+            zn = rz[ix1];
+            an = ra[ix1];
+          }
+          fresh = bend && !triv && k >= lim;
         }
       }
     }
