@@ -373,6 +373,41 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
       if (!done && k < avail_hi) {
         zn = s_at(k, lo_pos);
         an = k < m - 1 ? a_at(k, lo_pos) : 0.0;
+        // The first gate after a restart pushes one point on both hulls and
+        // cannot bend unless it ends the piece (zero weight, chain end), so it
+        // is taken here with the same operations instead of in a trip of its
+        // own.  Entry 0 of a hull lives in registers only.
+        if (bk >= 0 && k + 1 < pe && an != 0.0) {
+          ++k;
+          const double v1 = zn;
+          sk += v1;
+          ref = v1;
+          tot += v1;
+          alleq = alleq && (v1 == ref);
+          const double u1 = sk + an, l1 = sk - an;
+          c0x = k;
+          c0y = u1;
+          tc0 = tot;
+          ec0 = alleq;
+          ct2x = i0;
+          ct2y = a_val;
+          ct1x = k;
+          ct1y = u1;
+          nc = 1;
+          f0x = k;
+          f0y = l1;
+          tf0 = tot;
+          ef0 = alleq;
+          ft2x = i0;
+          ft2y = a_val;
+          ft1x = k;
+          ft1y = l1;
+          nf = 1;
+          if (k < avail_hi) {
+            zn = s_at(k, lo_pos);
+            an = k < m - 1 ? a_at(k, lo_pos) : 0.0;
+          }
+        }
       }
     }
   };
