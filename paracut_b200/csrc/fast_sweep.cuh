@@ -31,6 +31,7 @@
 // anchor falls behind the ring reads and writes those positions in global
 // memory; retirement is masked by each lane's emitted frontier.
 #pragma once
+#include <cuda.h>  // CUtensorMap
 #include <type_traits>
 
 namespace pcb {
@@ -78,6 +79,49 @@ struct Args {
   int nb;
   int export_g;     // LAST: also store the per-node g = sum_j d_j (fp32) in G
 };
+
+// TMA descriptors of one family launch.  Strided families (cols, 3D y / z)
+// whose warps' 32 chains are 32 consecutive nodes at every position load
+// their ring tiles -- p_j and the weights (interleaved [pos][C]) and the
+// drift c (natural layout) -- as (32 chains x 8 positions) boxes, one
+// instruction per array per tile, completing on a per-tile mbarrier.
+struct Maps {
+  CUtensorMap p, a, c;
+  int tma;      // 1: use the maps (else cp.async per lane)
+  int c3;       // the c map is 3D: (x = c % cdiv, pos, c / cdiv)
+};
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(unsigned dst, const CUtensorMap* map, int x, int y,
+                                      unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(unsigned dst, const CUtensorMap* map, int x, int y, int z,
+                                      unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
 
 // Predicated copies (no zero fill): slots of positions past the chain end or
 // of lanes without a chain are never read, so skipping them is enough and
@@ -133,10 +177,19 @@ __device__ __forceinline__ double rcp_r<double>(int di) {
 // ALU-pipe bound)
 __device__ __forceinline__ int rix(int l, int pos) { return (pos & (RL - 1)) ^ ((l << 5) | l); }
 
+// [pos][lane] ring index ((pos & 31) << 5) | l as one LOP3 on pos << 5 (the
+// shift is an IMAD on the FMA pipe; the scan is ALU-pipe bound)
+__device__ __forceinline__ int pix(int l, int pos) {
+  int r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(pos << 5), "r"((RL - 1) << 5), "r"(l));
+  return r;
+}
+
 template <int ROLE>
 __host__ __device__ constexpr int ring_bytes_host() {
-  // rz f64, rp f32, ra f32 (+ rf f64 for SHADOW)
-  return 32 * RL * (8 + 4 + 4 + (ROLE == SHADOW ? 8 : 0));
+  // rz f64, rp f32, ra f32 (+ rf f64 for SHADOW), + NT tile mbarriers, padded
+  // to 128 B so every warp's tile slots stay TMA-aligned
+  return 32 * RL * (8 + 4 + 4 + (ROLE == SHADOW ? 8 : 0)) + 128;
 }
 
 // lagging-lane accessors (positions below the ring), kept out of line
@@ -176,8 +229,9 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
 }
 
 template <int ROLE, bool ROWLIKE>
-__global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+__global__ void __launch_bounds__(WARPS * 32)
+    k_sweep(const __grid_constant__ Args A, const __grid_constant__ Maps M) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];  // TMA boxes land 128-B aligned
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const Fam F = A.F;
@@ -189,6 +243,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   double* rf = rz + 32 * RL;  // SHADOW only
   float* rp = reinterpret_cast<float*>(base + 32 * RL * (ROLE == SHADOW ? 16 : 8));
   float* ra = rp + 32 * RL;
+  // ring layout: [pos][lane] rows of 32 for strided families (every access is
+  // lane-contiguous, and a (positions x 32 chains) box is one contiguous
+  // block); row-like families keep [lane][pos] with the XOR swizzle that
+  // their 8-lanes-along-a-row loads need
+  auto rx = [](int l, int pos) { return ROWLIKE ? rix(l, pos) : pix(l, pos); };
+  const bool use_tma = !ROWLIKE && M.tma;
+  unsigned long long* mbar =
+      reinterpret_cast<unsigned long long*>(base + 32 * RL * (ROLE == SHADOW ? 24 : 16));
 
   const bool warp_live = c0 < F.C;
   const int nvalid = warp_live ? (int)min((int64_t)32, F.C - c0) : 0;
@@ -265,6 +327,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   int pre_tile = -1;
 
   int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
+  const int cx0 = (int)(c0 % F.cdiv), co0 = (int)(c0 / F.cdiv);  // TMA box origin of c
+  if (use_tma && warp_live) {
+    if (lane == 0) {
+      for (int u = 0; u < NT; ++u) mbar_init((unsigned)__cvta_generic_to_shared(&mbar[u]), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncwarp();
+  }
+  // tile T has landed (TMA: its mbarrier; cp.async: all but the newer groups)
+  auto land = [&](int T) {
+    if (use_tma) {
+      const int u = T - t_first;
+      mbar_wait((unsigned)__cvta_generic_to_shared(&mbar[u & (NT - 1)]), (unsigned)((u / NT) & 1));
+    } else {
+      cp_wait(t_ld - T - 1);
+    }
+    __syncwarp();
+  };
   if (has && start > 0 && stouch != 0)  // anchored on a tube touch: skr = -touch * a(start-1)
     skr = (R)(-(double)stouch * (double)A.wf[((start - 1) * C32 + c32)]);
   // end value offset at `stop`: the string ends at S_stop + touch * a(stop-1)
@@ -274,16 +354,31 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   auto issue = [&](int T) {
     const int k0 = T * TP;
     PCB_CNT(3, 1);
+    if (use_tma) {  // one elected lane moves the three (8 x 32) boxes of the tile
+      if (lane == 0) {
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(&mbar[(T - t_first) & (NT - 1)]);
+        const int slot = (T & (NT - 1)) * TP * 32;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // ring was read generically
+        mbar_expect(bar, TP * 32 * (4 + 4 + 8));
+        tma2d((unsigned)__cvta_generic_to_shared(rp + slot), &M.p, (int)c0, k0, bar);
+        tma2d((unsigned)__cvta_generic_to_shared(ra + slot), &M.a, (int)c0, k0, bar);
+        if (M.c3)
+          tma3d((unsigned)__cvta_generic_to_shared(rz + slot), &M.c, cx0, k0, co0, bar);
+        else
+          tma2d((unsigned)__cvta_generic_to_shared(rz + slot), &M.c, (int)c0, k0, bar);
+      }
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < TP; ++q) {  // mode A
       const int pos = k0 + q;
       const bool pr = valid && pos < m;
       const int fi = pr ? (pos * C32 + c32) : 0;
-      cp4(&rp[rix(lane, pos)], A.p + fi, pr);
-      cp4(&ra[rix(lane, pos)], A.wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
+      cp4(&rp[rx(lane, pos)], A.p + fi, pr);
+      cp4(&ra[rx(lane, pos)], A.wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
       if (!ROWLIKE) {
         const int nd = pr ? node(base32, pos) : 0;
-        cp8(&rz[rix(lane, pos)], A.c + nd, pr);
+        cp8(&rz[rx(lane, pos)], A.c + nd, pr);
       }
     }
     if (ROWLIKE) {  // mode B: lanes 8g..8g+7 along chain rows {8g + ib}
@@ -295,7 +390,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         const int bi = bB[ib];
         const bool pr = i < nvalid && pos < m;
         const int nd = pr ? node(bi, pos) : 0;
-        cp8(&rz[rix(i, pos)], A.c + nd, pr);
+        cp8(&rz[rx(i, pos)], A.c + nd, pr);
       }
     }
     cp_commit();
@@ -333,7 +428,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
   auto to_z = [&](int T) {
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
-      const int ix = rix(lane, T * TP + q);
+      const int ix = rx(lane, T * TP + q);
       rz[ix] = (double)rp[ix] + rz[ix];
     }
   };
@@ -348,7 +443,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       const int pos = k0 + q;
       if (has && pos >= start && pos < stop && pos < i0) {
         const int slot = pos & (RL - 1);
-        const int ix = rix(lane, pos);
+        const int ix = rx(lane, pos);
         const double zj = rz[ix];
         if ((smask >> slot) & 1u) {
           zs = zj;
@@ -400,7 +495,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         const unsigned em_i = __shfl_sync(0xffffffffu, emask, i);
         const int bi = bB[ib];
         if ((em_i >> q) & 1u) {
-          const int ix = rix(i, pos);
+          const int ix = rx(i, pos);
           const int nd = node(bi, pos);
           if (ROLE == SHADOW) {
             A.y[nd] = rz[ix];
@@ -432,8 +527,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
     asm volatile("" : "+r"(keep_min));  // keep it in a register, not re-derived per trip
     // software-pipelined ring reads: the next gate's z and a are loaded at the
     // end of the previous trip (slots >= k are never written by the scan)
-    double zn = rz[rix(lane, k)];
-    float an = ra[rix(lane, k)];
+    double zn = rz[rx(lane, k)];
+    float an = ra[rx(lane, k)];
     const int lim = min(avail_hi, stop);  // gates are consumed while k < lim
     if (!LAG && fresh && k < lim) {  // first gate of the unit or after a lagging round
       t = zn;
@@ -497,7 +592,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         const int bk = tf ? f0x : (tc ? c0x : k);
         const R fill = tf ? fs : (tc ? cs : sE * inv);
         // ---- close segment [i0, bk): its prox value is the string slope `fill` (+ t)
-        R ab = (R)ra[rix(lane, bk - 1)];
+        R ab = (R)ra[rx(lane, bk - 1)];
         int s0 = i0;
         R qv = -fill;  // q = z_i0 - fill, and z_i0 - t = 0
         if (LAG && bend && i0 < lo_pos) {
@@ -507,10 +602,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
           for (int j = i0; j < e2; ++j)
             nrm += finish_global<ROLE>(A, (j * C32 + c32), node(base32, j), fabs_);
           s0 = e2;
-          if (s0 < bk) qv = (R)((rz[rix(lane, s0)] - t) - (double)fill);
+          if (s0 < bk) qv = (R)((rz[rx(lane, s0)] - t) - (double)fill);
         }
         const bool mark = bend && s0 < stop && (!LAG || s0 < bk);
-        const int ixs = rix(lane, s0);
+        const int ixs = rx(lane, s0);
         if (mark) {
           if (ROLE == SHADOW) rf[ixs] = (double)qv;
           else ra[ixs] = (float)qv;
@@ -526,7 +621,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         // c0x / f0x = -1 make the next gate overwrite cs, Lc, fs, Lf
         c0x = bend ? -1 : c0x;
         f0x = bend ? -1 : f0x;
-        const int ixn = rix(lane, k);
+        const int ixn = rx(lane, k);
         zn = rz[ixn];
         an = ra[ixn];
         // non-lagging: the anchor value of a restarted string is the next gate's
@@ -549,7 +644,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
             fs = skr - rk1;
             Lf = fs;
             k = k1;
-            const int ix1 = rix(lane, k1);
+            const int ix1 = rx(lane, k1);
             zn = rz[ix1];
             an = ra[ix1];
           }
@@ -561,8 +656,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
 
   if (warp_live && rhi > 0) {
     while (t_ld < ntiles && t_ld - t_first < NT) issue(t_ld++);
-    cp_wait(t_ld - t_first - 1);
-    __syncwarp();
+    land(t_first);
     to_z(t_first);
     t_rdy = t_first + 1;
     for (;;) {
@@ -580,8 +674,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
         scan(lo_pos, avail_hi, keep, std::false_type());
       __syncwarp();
       if (__all_sync(0xffffffffu, i0 >= stop)) {
-        cp_wait(0);
-        __syncwarp();
+        if (use_tma) {
+          for (int T = t_rdy; T < t_ld; ++T) land(T);  // no TMA may be in flight at exit
+        } else {
+          cp_wait(0);
+          __syncwarp();
+        }
         for (int T = t_lo; T < t_ld; ++T) retire(T);
         break;
       }
@@ -594,8 +692,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_sweep(Args A) {
       __syncwarp();
       while (t_ld < ntiles && t_ld - t_lo < NT) issue(t_ld++);
       if (t_rdy < t_ld) {
-        cp_wait(t_ld - t_rdy - 1);
-        __syncwarp();
+        land(t_rdy);
         to_z(t_rdy);
         ++t_rdy;
       }

@@ -759,6 +759,7 @@ struct pcb_solver {
   DBuf<double> z;      // F64: r*n AAR point
   DBuf<double> y;      // r*n shadow (both modes)
   DBuf<float> p32;     // F32: r*n shadow state
+  pcb::fast::Maps maps[MAXR]{};  // F32: TMA descriptors of the strided families
   DBuf<double> cdrift; // F32: n drift
   DBuf<float> X32;     // F32: primal
   DBuf<float> G32;     // F32: accumulator
@@ -1101,7 +1102,7 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
 }
 
 template <int ROLE, bool ROWLIKE>
-int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
+int launch_sweep(pcb_solver* h, const pcb::fast::Args& a, const pcb::fast::Maps& M) {
   const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>();
   // set once per device (outside any later CUDA-graph capture of the sweep)
   static unsigned set_mask = 0;
@@ -1113,14 +1114,15 @@ int launch_sweep(pcb_solver* h, const pcb::fast::Args& a) {
   }
   const int per = pcb::fast::WARPS * 32;
   const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
-  pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a);
+  pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a, M);
   LAUNCH_CHECK(h);
   return 0;
 }
 
 template <int ROLE>
-int launch_role(pcb_solver* h, const pcb::fast::Args& a) {
-  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a) : launch_sweep<ROLE, false>(h, a);
+int launch_role(pcb_solver* h, const pcb::fast::Args& a, int j) {
+  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a, h->maps[j])
+                               : launch_sweep<ROLE, false>(h, a, h->maps[j]);
 }
 
 // merge points of family j for the current state (before its sweep)
@@ -1141,6 +1143,81 @@ int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) {
   a.merge = h->merge.p;
   a.nb = h->nbk[j];
   return 0;
+}
+
+// cuTensorMapEncodeTiled from the driver (no -lcuda link needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    else
+      (void)cudaGetLastError();
+  }
+  return fn;
+}
+
+// TMA maps for the strided families whose warps cover 32 consecutive nodes
+// (cols; 3D y with D2 % 32 == 0; 3D z).  Others keep the per-lane cp.async.
+// PCB_TMA=0 disables them.
+void build_maps(pcb_solver* h) {
+  for (int j = 0; j < MAXR; ++j) h->maps[j] = pcb::fast::Maps{};
+  const char* env = getenv("PCB_TMA");
+  if (env && env[0] == '0') return;
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return;
+  using pcb::fast::TP;
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    if (fam_rowlike(F.kind) || F.zz != 0 || F.C % 32 != 0 || F.m < 2) continue;
+    bool c3;
+    if (F.cdiv == 1 && F.chi == 1 && F.clo == 0)
+      c3 = false;  // node = c + i * ns
+    else if (F.clo == 1 && F.cdiv % 32 == 0)
+      c3 = true;  // node = (c / cdiv) * chi + c % cdiv + i * ns
+    else
+      continue;
+    pcb::fast::Maps M{};
+    const cuuint32_t box2[2] = {32, (cuuint32_t)TP}, es2[2] = {1, 1};
+    const cuuint64_t dp[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
+    const cuuint64_t da[2] = {(cuuint64_t)F.C, (cuuint64_t)(F.m - 1)};
+    const cuuint64_t sp[1] = {(cuuint64_t)F.C * 4};
+    CUresult r1 = fn(&M.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(h->p32.p + (int64_t)j * h->n), dp, sp, box2, es2,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r2 = fn(&M.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)h->wf32[j].p, da, sp, box2,
+                     es2, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r3;
+    if (!c3) {
+      const cuuint64_t dc[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
+      const cuuint64_t sc[1] = {(cuuint64_t)F.ns * 8};
+      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)h->cdrift.p, dc, sc, box2, es2,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      const cuuint64_t dc[3] = {(cuuint64_t)F.cdiv, (cuuint64_t)F.m, (cuuint64_t)(F.C / F.cdiv)};
+      const cuuint64_t sc[2] = {(cuuint64_t)F.ns * 8, (cuuint64_t)F.chi * 8};
+      const cuuint32_t box3[3] = {32, (cuuint32_t)TP, 1}, es3[3] = {1, 1, 1};
+      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)h->cdrift.p, dc, sc, box3, es3,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) continue;
+    M.tma = 1;
+    M.c3 = c3 ? 1 : 0;
+    h->maps[j] = M;
+  }
 }
 
 int fam_units(const pcb_solver* h, int j) {
@@ -1179,9 +1256,9 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     prof_begin(h, j);
     int rc = launch_merge(h, j, a);
     if (!rc) {
-      if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a);
-      else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a);
-      else rc = launch_role<pcb::fast::LAST>(h, a);
+      if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a, j);
+      else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a, j);
+      else rc = launch_role<pcb::fast::LAST>(h, a, j);
     }
     prof_end(h);
     if (rc) return rc;
@@ -1212,7 +1289,7 @@ int shadow_fast(pcb_solver* h) {
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
                       nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p, nullptr, 1, 0};
     if (int rc = launch_merge(h, j, a)) return rc;
-    if (int rc = launch_role<pcb::fast::SHADOW>(h, a)) return rc;
+    if (int rc = launch_role<pcb::fast::SHADOW>(h, a, j)) return rc;
   }
   return 0;
 }
@@ -1346,6 +1423,7 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
     if ((rc = h->G32.alloc(n))) return bail(rc);
     phase("alloc");
     if ((rc = ensure_wf32(h))) return bail(rc);
+    build_maps(h);
     phase("family weights");
     if ((rc = choose_split(h))) return bail(rc);
     phase("split");
