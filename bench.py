@@ -380,13 +380,16 @@ def main():
     nedge = [int(np.count_nonzero(a)) for a in g.dir_weights]
     fam_edges = _family_edges(g)
     per_launch = b * (2 * n + fam_edges[fam])
+    if precision == "f64":  # the exact sweep is one launch over all families
+        per_launch = sum(b * (2 * n + e) for e in fam_edges)
     mean_ms = fam_ms[fam] / max(int(fam_cnt[fam]), 1)
     achieved = per_launch / (mean_ms / 1e3) / 1e9
     traffic = _ncu_traffic(args.workload, fam)
     B_iter = algorithmic_bytes(g, r, b)
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
             "frac": achieved / pk, "traffic": traffic,
-            "kernel": "family %d (%s) prox sweep" % (fam, pc.decompose_grid(g).families[fam]),
+            "kernel": ("exact prox sweep, all families in one launch" if precision == "f64"
+                       else "family %d (%s) prox sweep" % (fam, pc.decompose_grid(g).families[fam])),
             "bytes_per_launch": per_launch, "mean_launch_ms": mean_ms,
             "share_of_step": float(fam_ms[fam] / ms) if ms > 0 else None,
             "peak_kind": pk_kind,
@@ -409,10 +412,15 @@ def main():
         cfg = pc.SolverConfig(algorithm="aar", max_iters=args.steps,
                               check_every=args.steps + 1, precision=precision,
                               device=local)
-        t0 = time.perf_counter()
-        res = pc.solve(g, pc.decompose_grid(g), cfg)
-        _ = res.labeling.sum()
-        wall = time.perf_counter() - t0
+        walls = []
+        res = None
+        for _rep in range(3):  # median of three end-to-end solves
+            res = None  # release the previous solve's device state first
+            t0 = time.perf_counter()
+            res = pc.solve(g, pc.decompose_grid(g), cfg)
+            _ = res.labeling.sum()
+            walls.append(time.perf_counter() - t0)
+        wall = float(np.median(walls))
         wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(wt, op=dist.ReduceOp.MAX)
@@ -421,7 +429,8 @@ def main():
         d2h = n + 8 * n + 2 * nb + 2 * 8 * 4
         e2e = {"value": world * r * n * args.steps / wall, "unit": "updates/s",
                "h2d_bytes_per_step": wbytes / args.steps, "d2h_bytes_per_step": d2h / args.steps,
-               "wall_s": wall, "certified": bool(res.certified), "gap": float(res.gap)}
+               "wall_s": wall, "wall_s_runs": walls, "certified": bool(res.certified),
+               "gap": float(res.gap)}
 
     if rank == 0:
         line = {

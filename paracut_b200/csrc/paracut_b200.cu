@@ -984,9 +984,8 @@ bool exact_thread_kernel() {
 }
 
 // exact prox of families j0..j1-1: srcs[j-j0] -> dsts[j-j0] (n each).  The
-// families are independent and go out as one launch (blockIdx.y = family),
-// except under profiling, where each family is its own launch for
-// per-family timing.
+// families are independent and go out as one launch (blockIdx.y = family);
+// under profiling that launch is timed as family j0.
 int sweep_exact_sel(pcb_solver* h, int j0, int j1, const double* const* srcs,
                     double* const* dsts, bool zero_singletons = false) {
   const Spill sp = spill_of(h);
@@ -1023,18 +1022,6 @@ int sweep_exact_sel(pcb_solver* h, int j0, int j1, const double* const* srcs,
     return deep ? launch_exact_sweep<32>(h, S, nfam, maxC)
                 : launch_exact_sweep<16>(h, S, nfam, maxC);
   };
-  if (h->profiling) {
-    for (int j = j0; j < j1; ++j) {
-      if (h->fam[j].C == 0) continue;
-      pcb::exact::ArgSet S{};
-      S.f[0] = args_of(j);
-      prof_begin(h, j);
-      if (int e = launch(S, 1, h->fam[j].C)) return e;
-      prof_end(h);
-      LAUNCH_CHECK(h);
-    }
-    return 0;
-  }
   pcb::exact::ArgSet S{};
   int64_t maxC = 0;
   for (int j = j0; j < j1; ++j) {
@@ -1042,7 +1029,9 @@ int sweep_exact_sel(pcb_solver* h, int j0, int j1, const double* const* srcs,
     maxC = h->fam[j].C > maxC ? h->fam[j].C : maxC;
   }
   if (maxC == 0) return 0;
+  prof_begin(h, j0);  // one launch for all families: timed as family j0
   if (int e = launch(S, j1 - j0, maxC)) return e;
+  prof_end(h);
   LAUNCH_CHECK(h);
   return 0;
 }
