@@ -77,6 +77,16 @@ int pcb_project_L(const double *w, const int64_t *degree, const uint8_t *support
  * graph.direction_shape. */
 int pcb_create(const int64_t *dims, int ndim, int conn, int precision, const double *w,
                const double *const *dir_weights, int device, pcb_solver **out);
+/* Device ingest of a PCUT1B grid file (reference io.py:143-224 layout:
+ * "PCUT1B", connectivity code u8, ndim u8, dims u64 LE, then w and each
+ * direction array as LE fp64): the payload streams from the file through
+ * pinned staging buffers into the handle's device arrays, with no host copy
+ * of the instance.  Same handle as pcb_create; dims_out (3 entries), ndim_out
+ * and conn_out (nullable) report the header.  PCB_E_ARG on a malformed file
+ * (the reference's ValueError cases: bad magic, connectivity code, dimension
+ * count, truncated header or payload). */
+int pcb_create_from_file(const char *path, int precision, int device, pcb_solver **out,
+                         int64_t *dims_out, int *ndim_out, int *conn_out);
 int pcb_destroy(pcb_solver *h);
 /* Device memory of destroyed handles stays mapped in a per-device pool for
  * the next handle; this returns it to the driver. */

@@ -66,6 +66,7 @@ def _declare(L):
     L.pcb_level_set.argtypes = [P, P, P, P]
     L.pcb_dual_init.argtypes = [P, INT, P]
     L.pcb_release_memory.argtypes = [INT]
+    L.pcb_create_from_file.argtypes = [ctypes.c_char_p, INT, INT, P, P, P, P]
     L.pcb_debug_counters.argtypes = [P, INT]
     L.pcb_dual_run.argtypes = [P, I64, P, P]
     L.pcb_project_K.argtypes = [P, P, P]
@@ -83,7 +84,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
-           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
 
 
@@ -151,6 +152,16 @@ class GridSolver:
         self.device = int(device)
         self.dims = tuple(int(d) for d in g.dims)
         dims = np.asarray(self.dims, dtype=np.int64)
+        if getattr(g, "_is_grid_file", False):
+            # device ingest: the payload goes file -> pinned staging -> HBM
+            h = P()
+            check(L.pcb_create_from_file(os.fsencode(g.path), PRECISIONS[precision],
+                                         self.device, ctypes.byref(h), None, None, None))
+            self._h = h
+            r, n = INT(0), I64(0)
+            check(L.pcb_shape(h, ctypes.byref(r), ctypes.byref(n)))
+            self.r, self.n = int(r.value), int(n.value)
+            return
         w = _f64(g.w)
         dws = [_f64(a) for a in g.dir_weights]
         arr = (P * 4)(*([ptr(a) for a in dws] + [None] * (4 - len(dws))))

@@ -28,6 +28,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cerrno>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -1340,9 +1344,58 @@ int pcb_device_count(int* count) {
   return 0;
 }
 
-int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const double* w,
-               const double* const* dir_weights, int device, pcb_solver** out) {
-  if (!out || !dims || !w || !dir_weights) return fail(PCB_E_ARG, "null argument");
+}  // extern "C"
+
+namespace {
+
+// Weights source of a handle build: host arrays or a PCUT1B file.
+struct WeightSource {
+  const double* w = nullptr;
+  const double* const* dirw = nullptr;
+  int fd = -1;            // file: payload at `off` (w, then each direction array)
+  int64_t off = 0;
+};
+
+// pread `bytes` at `off` of fd into device memory through the pinned ring
+// (reads of chunk i+1 overlap the copy engine's chunk i)
+cudaError_t file_h2d(void* dst, int fd, int64_t off, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  hostio::Stage& S = hostio::stage();
+  std::lock_guard<std::mutex> lk(S.m);
+  if (!S.init()) return cudaErrorMemoryAllocation;
+  cudaEvent_t ev[hostio::SLOTS] = {};
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < hostio::SLOTS && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+  bool used[hostio::SLOTS] = {};
+  size_t i = 0;
+  for (size_t done = 0; done < bytes && e == cudaSuccess; done += hostio::CHUNK, ++i) {
+    const int slot = (int)(i % hostio::SLOTS);
+    const size_t len = bytes - done < hostio::CHUNK ? bytes - done : hostio::CHUNK;
+    if (used[slot]) e = cudaEventSynchronize(ev[slot]);
+    if (e != cudaSuccess) break;
+    size_t got = 0;
+    while (got < len) {
+      const ssize_t r = pread(fd, (char*)S.slot[slot] + got, len - got, (off_t)(off + done + got));
+      if (r <= 0) {
+        e = cudaErrorUnknown;
+        break;
+      }
+      got += (size_t)r;
+    }
+    if (e != cudaSuccess) break;
+    e = cudaMemcpyAsync((char*)dst + done, S.slot[slot], len, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaEventRecord(ev[slot], st);
+    used[slot] = true;
+  }
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  for (int k = 0; k < hostio::SLOTS; ++k)
+    if (ev[k]) cudaEventDestroy(ev[k]);
+  return e != cudaSuccess ? e : e2;
+}
+
+int create_impl(const int64_t* dims, int ndim, int conn, int precision, const WeightSource& src,
+                int device, pcb_solver** out) {
   *out = nullptr;
   if (conn < 0 || conn > 2) return fail(PCB_E_ARG, "unsupported connectivity code %d", conn);
   const int want_nd = conn == PCB_CONN_3D6 ? 3 : 2;
@@ -1385,16 +1438,24 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
   phase("set_dev");
   setup_geometry(h);
   if ((rc = h->w.alloc(n))) return bail(rc);
-  cudaError_t e = hostio::h2d(h->w.p, w, n * sizeof(double), 0);
+  int64_t foff = src.off;
+  cudaError_t e = src.fd >= 0 ? file_h2d(h->w.p, src.fd, foff, n * sizeof(double), 0)
+                              : hostio::h2d(h->w.p, src.w, n * sizeof(double), 0);
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "upload w: %s", cudaGetErrorString(e)));
+  foff += n * (int64_t)sizeof(double);
   for (int k = 0; k < h->DG.ndir; ++k) {
     const int64_t cnt = dir_size(h, k);
     if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
     if (cnt > 0) {
-      if (!dir_weights[k]) return bail(fail(PCB_E_ARG, "direction %d weights are null", k));
-      e = hostio::h2d(h->dirw[k].p, dir_weights[k], cnt * sizeof(double), 0);
+      if (src.fd >= 0) {
+        e = file_h2d(h->dirw[k].p, src.fd, foff, cnt * sizeof(double), 0);
+      } else {
+        if (!src.dirw[k]) return bail(fail(PCB_E_ARG, "direction %d weights are null", k));
+        e = hostio::h2d(h->dirw[k].p, src.dirw[k], cnt * sizeof(double), 0);
+      }
       if (e != cudaSuccess)
         return bail(fail(PCB_E_CUDA, "upload weights: %s", cudaGetErrorString(e)));
+      foff += cnt * (int64_t)sizeof(double);
     }
   }
   phase("upload");
@@ -1429,6 +1490,73 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
   phase("rest");
   *out = h;
   return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const double* w,
+               const double* const* dir_weights, int device, pcb_solver** out) {
+  if (!out || !dims || !w || !dir_weights) return fail(PCB_E_ARG, "null argument");
+  WeightSource src;
+  src.w = w;
+  src.dirw = dir_weights;
+  return create_impl(dims, ndim, conn, precision, src, device, out);
+}
+
+int pcb_create_from_file(const char* path, int precision, int device, pcb_solver** out,
+                         int64_t* dims_out, int* ndim_out, int* conn_out) {
+  if (!path || !out) return fail(PCB_E_ARG, "null argument");
+  *out = nullptr;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(PCB_E_ARG, "%s: cannot open (%s)", path, strerror(errno));
+  struct Closer {
+    int fd;
+    ~Closer() { close(fd); }
+  } closer{fd};
+  unsigned char head[8];
+  if (pread(fd, head, 8, 0) != 8) return fail(PCB_E_ARG, "%s: truncated header", path);
+  if (memcmp(head, "PCUT1B", 6) != 0) return fail(PCB_E_ARG, "%s: not a binary grid file", path);
+  const int code = head[6], ndim = head[7];
+  if (code > 2) return fail(PCB_E_ARG, "%s: unknown connectivity code %d", path, code);
+  if (ndim != (code == PCB_CONN_3D6 ? 3 : 2))
+    return fail(PCB_E_ARG, "%s: dimension count does not match connectivity", path);
+  uint64_t d64[3] = {1, 1, 1};
+  if (pread(fd, d64, 8 * ndim, 8) != 8 * ndim) return fail(PCB_E_ARG, "%s: truncated header", path);
+  int64_t dims[3] = {1, 1, 1};
+  int64_t nodes = 1;
+  for (int a = 0; a < ndim; ++a) {  // little-endian u64 (x86 / Grace hosts)
+    if (d64[a] < 1 || d64[a] > ((uint64_t)1 << 30)) return fail(PCB_E_ARG, "%s: bad dimension", path);
+    dims[a] = (int64_t)d64[a];
+    nodes *= dims[a];
+  }
+  // payload size: w plus every direction array (sizes as direction_shape)
+  static const int offs[3][4][3] = {{{0, 1, 0}, {1, 0, 0}, {0, 0, 0}, {0, 0, 0}},
+                                    {{0, 1, 0}, {1, 0, 0}, {1, 1, 0}, {1, 1, 0}},
+                                    {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {0, 0, 0}}};
+  const int ndir = code == 1 ? 4 : (code == 0 ? 2 : 3);
+  int64_t count = nodes;
+  for (int k = 0; k < ndir; ++k) {
+    int64_t c = 1;
+    for (int a = 0; a < ndim; ++a) {
+      const int64_t len = dims[a] - offs[code][k][a];
+      c *= len > 0 ? len : 0;
+    }
+    count += c;
+  }
+  struct stat st;
+  if (fstat(fd, &st) != 0) return fail(PCB_E_ARG, "%s: cannot stat", path);
+  const int64_t off = 8 + 8 * (int64_t)ndim;
+  if ((int64_t)st.st_size != off + 8 * count) return fail(PCB_E_ARG, "%s: truncated payload", path);
+  WeightSource src;
+  src.fd = fd;
+  src.off = off;
+  if (dims_out)
+    for (int a = 0; a < ndim; ++a) dims_out[a] = dims[a];
+  if (ndim_out) *ndim_out = ndim;
+  if (conn_out) *conn_out = code;
+  return create_impl(dims, ndim, code, precision, src, device, out);
 }
 
 int pcb_debug_counters(uint64_t* out, int reset) {

@@ -211,3 +211,48 @@ def decompose_grid(g):
         except ValueError:
             raise ValueError("chain decomposition requires a grid instance")
     return GridDecomposition(g)
+
+
+def validate(dec, g, rng=None, report=None):
+    """Decomposition invariants against the grid (decompose.py:203-260 checks).
+
+    Every class partitions the nodes, the chain edges of all classes are the
+    grid's positive edges exactly once with their weights, and
+    sum_j f_j(x) = f(x) on random vectors (relative 1e-10).  Returns a bool;
+    diagnostics go to ``report`` (a list) when given.
+    """
+    problems = []
+    lo_all, hi_all, a_all = [], [], []
+    for k, cls in enumerate(dec.classes):
+        if np.unique(cls.node_idx).size != cls.node_idx.size:
+            problems.append("class %d: chains share a vertex" % k)
+        if cls.node_idx.size != g.n:
+            problems.append("class %d: chains do not partition every node" % k)
+        ei, ej, ea = cls.edge_pairs()
+        if ea.size and ea.min() <= 0:
+            problems.append("class %d: nonpositive chain edge weight" % k)
+        lo_all.append(np.minimum(ei, ej))
+        hi_all.append(np.maximum(ei, ej))
+        a_all.append(np.asarray(ea, dtype=np.float64))
+    lo = np.concatenate(lo_all) if lo_all else np.zeros(0, np.int64)
+    hi = np.concatenate(hi_all) if hi_all else np.zeros(0, np.int64)
+    a = np.concatenate(a_all) if a_all else np.zeros(0)
+    order = np.lexsort((hi, lo))
+    lo, hi, a = lo[order], hi[order], a[order]
+    if lo.size > 1 and np.any((lo[1:] == lo[:-1]) & (hi[1:] == hi[:-1])):
+        problems.append("an edge appears in more than one chain")
+    gi, gj, ga = g.edge_arrays()
+    if lo.size != gi.size or not (np.array_equal(lo, gi) and np.array_equal(hi, gj)):
+        problems.append("chain edges do not match the grid edges")
+    elif not np.array_equal(a, ga):
+        problems.append("chain edge weights altered")
+    rng = np.random.default_rng(0) if rng is None else rng
+    for _ in range(3):
+        x = rng.normal(size=g.n)
+        f, fj = g.tv(x), sum(c.tv(x) for c in dec.classes)
+        if abs(f - fj) > 1e-10 * max(1.0, abs(f)):
+            problems.append("sum of class TVs %r differs from f(x) %r" % (fj, f))
+            break
+    if report is not None:
+        report.extend(problems)
+    return not problems

@@ -155,19 +155,94 @@ def tv_value(g, x):
 
 def instance_fingerprint(g):
     """sha256 over topology + pairwise weights (unaries excluded), as graph.py:195-213."""
+    fp = getattr(g, "_fingerprint", None)
+    if callable(fp):  # file-backed grids hash the payload without loading it
+        return fp()
     h = hashlib.sha256()
-    h.update(("grid:%s:%r" % (g.connectivity, tuple(g.dims))).encode())
-    for arr in g.dir_weights:
-        h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    if hasattr(g, "dims"):
+        h.update(("grid:%s:%r" % (g.connectivity, tuple(g.dims))).encode())
+        for arr in g.dir_weights:
+            h.update(np.ascontiguousarray(arr, dtype=np.float64).tobytes())
+    else:
+        h.update(("cut:%d" % g.n).encode())
+        h.update(np.ascontiguousarray(g.edge_i, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(g.edge_j, dtype=np.int64).tobytes())
+        h.update(np.ascontiguousarray(g.edge_a, dtype=np.float64).tobytes())
     return h.hexdigest()
 
 
 def as_grid(g):
     """Accept our GridEnergy or any object with the reference's grid fields."""
-    if isinstance(g, GridEnergy):
+    if isinstance(g, GridEnergy) or getattr(g, "_is_grid_file", False):
         return g
     for attr in ("dims", "connectivity", "w", "dir_weights"):
         if not hasattr(g, attr):
             raise ValueError("the B200 path needs a grid instance (dims, "
                              "connectivity, w, dir_weights)")
     return GridEnergy(g.dims, g.connectivity, g.w, g.dir_weights)
+
+
+class CutInstance:
+    """General (non-grid) cut instance, host only (reference graph.py:42-113).
+
+    The device path needs a grid; this class carries DIMACS instances through
+    the file formats and the small verification helpers.  Edges are stored
+    sorted by (i, j), i < j, positive weights only; duplicates are rejected.
+    """
+
+    def __init__(self, w, edges):
+        self.w = np.ascontiguousarray(w, dtype=np.float64)
+        if self.w.ndim != 1 or self.w.size < 1:
+            raise ValueError("w must be a nonempty 1D vector")
+        n = self.w.size
+        if len(edges) == 0:
+            e = np.zeros((0, 3))
+        else:
+            e = np.asarray(edges, dtype=np.float64).reshape(-1, 3)
+        i, j, a = e[:, 0].astype(np.int64), e[:, 1].astype(np.int64), np.ascontiguousarray(e[:, 2])
+        if np.any(a < 0):
+            raise ValueError("edge weights must be nonnegative")
+        lo, hi = np.minimum(i, j), np.maximum(i, j)
+        if np.any(lo < 0) or np.any(hi >= n) or np.any(lo == hi):
+            raise ValueError("edge endpoints out of bounds or self-loop")
+        pos = a > 0.0
+        lo, hi, a = lo[pos], hi[pos], a[pos]
+        order = np.lexsort((hi, lo))
+        self.edge_i = np.ascontiguousarray(lo[order])
+        self.edge_j = np.ascontiguousarray(hi[order])
+        self.edge_a = np.ascontiguousarray(a[order])
+        if self.edge_i.size > 1:
+            same = (self.edge_i[1:] == self.edge_i[:-1]) & (self.edge_j[1:] == self.edge_j[:-1])
+            if np.any(same):
+                raise ValueError("duplicate edges")
+
+    @property
+    def n(self):
+        return self.w.size
+
+    @property
+    def num_edges(self):
+        return self.edge_i.size
+
+    def edge_arrays(self):
+        return self.edge_i, self.edge_j, self.edge_a
+
+    def tv(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError("length mismatch")
+        if self.edge_i.size == 0:
+            return 0.0
+        return float(np.abs(x[self.edge_i] - x[self.edge_j]) @ self.edge_a)
+
+    def energy(self, x):
+        x = np.asarray(x, dtype=np.float64)
+        if x.shape != (self.n,):
+            raise ValueError("length mismatch")
+        return self.tv(x) - float(self.w @ x)
+
+    def scaled_pairwise(self, factor):
+        if factor < 0:
+            raise ValueError("scale factor must be nonnegative")
+        return CutInstance(self.w.copy(), np.column_stack([self.edge_i, self.edge_j,
+                                                           self.edge_a * factor]))

@@ -220,6 +220,7 @@ def main():
 
     make_levels()
     make_dual()
+    make_io()
 
 
 def make_levels():
@@ -296,7 +297,42 @@ def make_dual():
             save("dual_%s_%s.npz" % (alg, name), **d)
 
 
-if __name__ == "__main__" and "levels" in sys.argv[1:]:
+def make_io():
+    """Files written by the reference's io.py (io.py:113-261): our readers must
+    load them bitwise and our writers must reproduce their bytes."""
+    global _PC
+    pc = import_reference()
+    _PC = pc
+    from paracut.solvers import TraceRow
+    r = np.random.default_rng(31)
+    out = os.path.join(HERE, "io")
+    os.makedirs(out, exist_ok=True)
+    for conn, dims in (("2D-4", (5, 7)), ("2D-8", (4, 6)), ("3D-6", (3, 4, 5))):
+        g = pc.random_grid(dims, conn, r)
+        tag = conn.replace("-", "").lower()
+        pc.write_grid(g, os.path.join(out, "grid_%s.pcut" % tag))
+        pc.write_grid(g, os.path.join(out, "grid_%s.txt" % tag), text=True)
+        np.savez(os.path.join(out, "grid_%s_arrays.npz" % tag), w=g.w,
+                 **{"dw%d" % k: a for k, a in enumerate(g.dir_weights)},
+                 fingerprint=np.array(pc.instance_fingerprint(g)))
+    w = r.uniform(-3, 3, 9)
+    edges = [(i, j, float(r.uniform(0.01, 2.0))) for i in range(9) for j in range(i + 1, 9)
+             if r.random() < 0.4]
+    inst = pc.CutInstance(w, edges)
+    pc.write_dimacs(inst, os.path.join(out, "cut.max"))
+    ei, ej, ea = inst.edge_arrays()
+    np.savez(os.path.join(out, "cut_arrays.npz"), w=inst.w, ei=ei, ej=ej, ea=ea,
+             fingerprint=np.array(pc.instance_fingerprint(inst)))
+    st = pc.DualState(y=r.normal(size=(2, 6)), z=r.normal(size=(2, 6)), fingerprint="fp-io")
+    pc.save_dual(st, os.path.join(out, "state.dual"))
+    trace = [TraceRow(0, 1.25, -0.5, 3.0, np.nan, 0.001), TraceRow(10, 0.0, 2.0, -1.0, 0.25, 0.002)]
+    pc.write_trace(trace, os.path.join(out, "trace.csv"))
+    print("wrote", out)
+
+
+if __name__ == "__main__" and "io" in sys.argv[1:]:
+    make_io()
+elif __name__ == "__main__" and "levels" in sys.argv[1:]:
     make_levels()
 elif __name__ == "__main__" and "dual" in sys.argv[1:]:
     make_dual()
