@@ -20,9 +20,13 @@ across ranks as partial sums of squares.  Communication goes through a
 on CPU -- or ``LocalComm`` for P virtual ranks in one process), so the
 same driver runs multi-process and single-process.
 
-Scope this round: fixed-iteration AAR, cold/warm start, final z/y/x
-gathering.  Gap checks on sharded state (halo exchange of boundary labels)
-are next.
+Certificates stay sharded (``check``): each handle computes its shadow,
+the cross family's shadow moves pencil -> slab in one fp64 all-to-all, every
+slab handle certifies its own nodes and intra-slab edges with the device
+reductions (``pcb_check``), the cut across slab boundaries uses the next
+rank's first label plane, and the per-rank cut, unary, dual and smooth-dual
+partials are summed across ranks.  ``solve_sharded`` runs the reference
+driver loop (checks every ``check_every``, stop at ``gap_tol``) on top.
 """
 from __future__ import annotations
 
@@ -249,6 +253,55 @@ class ShardedAAR:
         tot = self.comm.all_sum([a.cpu().numpy() for a in acc])
         return np.sqrt(np.maximum(np.asarray(tot[0], dtype=np.float64), 0.0))
 
+    # ---------------------------------------------------------------- certificates
+    def _ybuf(self, h):
+        if hasattr(h, "host_buffer"):  # CPU emulation
+            import torch
+            return torch.from_numpy(h.host_buffer(self.N.BUF_Y))
+        ptr, cnt = h.device_buffer(self.N.BUF_Y)
+        return _wrap(ptr, cnt, np.float64, self._dev())
+
+    def check(self, thresholds=(0.0,)):
+        """Global (energies[T], gaps[T], smooth dual) of the current iterate;
+        labels stay on their ranks (slab handles' check state)."""
+        import torch
+        thr = np.asarray(thresholds, dtype=np.float64)
+        T = thr.size
+        P, dz, cp, plane = self.geo.P, self.geo.dz, self.geo.cp, self.geo.plane
+        ns, npn = self.geo.n_slab, self.geo.n_pencil
+        x = self.cross
+        for s, p in zip(self.slab, self.pencil):
+            s.shadow()
+            p.shadow()
+        # the cross family's shadow: pencil (D0, cp) -> slab (dz, P * cp)
+        sends = [self._ybuf(p)[x * npn:(x + 1) * npn].view(P, dz, cp) for p in self.pencil]
+        recvs = [torch.empty((P, dz, cp), dtype=torch.float64, device=self._dev())
+                 for _ in self.ranks]
+        self.comm.all_to_all(sends, recvs)
+        for s, rv in zip(self.slab, recvs):
+            self._ybuf(s)[x * ns:(x + 1) * ns].view(dz, P, cp).copy_(rv.transpose(0, 1))
+        # per-rank certificate of the slab (its nodes, its intra-slab edges)
+        a_b = np.asarray(self.g.dir_weights[x], dtype=np.float64).reshape(self.g.dims[0] - 1, plane)
+        firsts_local, local = [], []
+        for rk, s in zip(self.ranks, self.slab):
+            e, gp, smooth = s.check(thr)
+            labs = np.stack([s.check_labels(t) for t in range(T)]).astype(np.float64)
+            mine = np.zeros((P, T, plane))
+            mine[rk] = labs[:, :plane]  # this slab's first label plane, for rank rk - 1
+            firsts_local.append(mine)
+            local.append((rk, e, float(e[0] - gp[0]), float(smooth), labs[:, -plane:]))
+        firsts = self.comm.all_sum(firsts_local)[0]
+        parts = []
+        for rk, e, dual, smooth, last in local:
+            cut_b = np.zeros(T)
+            if rk < P - 1:  # edges between this slab's last plane and the next one's first
+                cut_b = np.abs(last - firsts[rk + 1]) @ a_b[(rk + 1) * dz - 1]
+            parts.append(np.concatenate([np.asarray(e, dtype=np.float64) + cut_b,
+                                         [dual, smooth]]))
+        tot = self.comm.all_sum(parts)[0]
+        energies, dual, smooth = tot[:T], tot[T], tot[T + 1]
+        return energies, energies - dual, smooth
+
     def capture(self):
         """Record one fused iteration (norms off) as a CUDA graph; replay it with
         ``run_graph``.  Every handle launches on the capture stream, torch's
@@ -301,3 +354,31 @@ class ShardedAAR:
                 out[j, z0:z1] = sl[t].reshape(self.geo.dz, plane)
             out[self.cross][:, self.geo.pencil_cols(rk)] = pe.reshape(D0, self.geo.cp)
         return out.reshape(self.r, -1)
+
+
+def solve_sharded(g, comm, ranks, backend, cfg, device=None):
+    """AAR over slab shards with sharded certificates (the reference loop,
+    solvers.py:272-307, checks every cfg.check_every, stop at cfg.gap_tol).
+
+    Returns (trace, iterations, best_gap, best_energy, certified); trace rows
+    are (k, gap, dual_objective, energy) of the threshold with the least gap.
+    """
+    from .solvers import GAP_SLACK
+    sh = ShardedAAR(g, comm, ranks, backend, device=device)
+    sh.init_cold()
+    thr = np.asarray(cfg.thresholds, dtype=np.float64)
+    trace, best_gap, best_e = [], np.inf, np.nan
+    k = 0
+    while True:
+        if k % cfg.check_every == 0 or k >= cfg.max_iters:
+            e, gp, smooth = sh.check(thr)
+            t = int(np.argmin(gp))
+            trace.append((k, float(gp[t]), float(smooth), float(e[t])))
+            if gp[t] < best_gap:
+                best_gap, best_e = float(gp[t]), float(e[t])
+            if gp[t] <= cfg.gap_tol + GAP_SLACK or k >= cfg.max_iters:
+                break
+        nxt = min((k // cfg.check_every + 1) * cfg.check_every, cfg.max_iters)
+        sh.run(nxt - k, norms=False)
+        k = nxt
+    return trace, k, best_gap, best_e, best_gap <= cfg.gap_tol + GAP_SLACK

@@ -11,7 +11,7 @@ import numpy as np
 from oracle import oracle as orc
 
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
-BUF_G, BUF_X, BUF_C, BUF_NORMS = 0, 1, 2, 4
+BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
 ORDER = {"2D-4": (0, 1), "3D-6": (0, 1, 2)}
 
 
@@ -28,9 +28,12 @@ class EmuSolver:
         self.X = np.zeros(self.n, np.float32)
         self.G = np.zeros(self.n, np.float32)
         self.norms = np.zeros(1)
+        self.y = np.zeros((self.r, self.n))
+        self.bits = None
 
     def host_buffer(self, which):
-        return {BUF_G: self.G, BUF_X: self.X, BUF_C: self.c, BUF_NORMS: self.norms}[which]
+        return {BUF_G: self.G, BUF_X: self.X, BUF_C: self.c, BUF_Y: self.y.reshape(-1),
+                BUF_NORMS: self.norms}[which]
 
     def set_family_mask(self, mask):
         self.mask = mask
@@ -108,8 +111,23 @@ class EmuSolver:
         self.c += (xn - gd) / self.r
 
     def shadow(self, want_y=True, want_s=False):
-        y = np.zeros((self.r, self.n))
         for j in range(self.r):
             if (self.mask >> j) & 1:
-                y[j] = self._prox_proj(j, self.p[j].astype(np.float64) + self.c)
-        return y, None
+                self.y[j] = self._prox_proj(j, self.p[j].astype(np.float64) + self.c)
+        return self.y.copy(), None
+
+    def check(self, thr):
+        """pcb_check on this handle's grid: per threshold energy over its own
+        edges, gap = energy - sum min(s - w, 0), smooth dual."""
+        s = self.y.sum(axis=0)
+        x = self.w - s
+        labs = (x[None, :] > np.asarray(thr)[:, None]).astype(np.uint8)
+        self.bits = labs
+        e = np.array([orc.grid_tv(self.g, lab) - float(self.w @ lab) for lab in labs])
+        d = s - self.w
+        dual = float(np.minimum(d, 0.0).sum())
+        smooth = 0.5 * float(self.w @ self.w) - 0.5 * float(d @ d)
+        return e, e - dual, smooth
+
+    def check_labels(self, t, packed=False):
+        return self.bits[t]

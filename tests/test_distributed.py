@@ -36,7 +36,8 @@ def _worker(rank, world, port, conn, dims, iters, q):
         norms = sh.run(iters)
         parts = sh.local_z()
         ys = sh.local_shadow()
-        q.put((rank, parts, ys, norms))
+        cert = sh.check((0.0, 1e-3))
+        q.put((rank, parts, ys, norms, cert))
     finally:
         dist.destroy_process_group()
 
@@ -78,7 +79,7 @@ def test_gloo_world2_matches_unsharded(conn, dims):
     sh.r = len(DIRECTIONS[conn])
     sh.cross = cross
     zparts, yparts = {}, {}
-    for _, parts, ys, _ in res:
+    for _, parts, ys, _, _ in res:
         zparts.update(parts)
         yparts.update(ys)
     z = sh.assemble(zparts)
@@ -88,8 +89,15 @@ def test_gloo_world2_matches_unsharded(conn, dims):
     scale = np.max(np.abs(z_ref))
     assert np.max(np.abs(z - z_ref)) <= 1e-9 * scale
     assert np.max(np.abs(y - y_ref)) <= 1e-9 * max(1.0, np.max(np.abs(y_ref)))
-    for _, _, _, norms in res:
+    for _, _, _, norms, _ in res:
         assert np.allclose(norms, ref_norms, rtol=1e-9)
+    # sharded certificate (labels stay on their ranks, boundary planes
+    # exchanged, partials summed) == the unsharded certificate
+    e_ref, gap_ref, smooth_ref = ref.check(np.array([0.0, 1e-3]))
+    for _, _, _, _, (e, gap, smooth) in res:
+        assert np.allclose(e, e_ref, rtol=1e-9, atol=1e-9)
+        assert np.allclose(gap, gap_ref, rtol=1e-9, atol=1e-9)
+        assert smooth == pytest.approx(smooth_ref, rel=1e-9, abs=1e-9)
 
 
 def test_geometry_partition():
@@ -167,3 +175,47 @@ def test_nccl_world1_and_graph_capture_match_eager():
     finally:
         dist.destroy_process_group()
     assert np.array_equal(z, z_ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,conn,dims", [(2, "3D-6", (16, 20, 24)), (4, "2D-4", (64, 48))])
+def test_virtual_ranks_sharded_certificate_matches_single(P, conn, dims):
+    """Sharded certificate (device shadows, fp64 transpose of the cross
+    shadow, per-slab pcb_check, boundary planes) == the single handle's
+    certificate of the same shadow."""
+    from paracut_b200 import _native
+    spec = {"2D-4": CONFIGS["cfg2_int"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=5, dims=dims)
+    sh = ShardedAAR(g, LocalComm(P), range(P),
+                    lambda sub: _native.GridSolver(sub, precision="f32"), device="cuda")
+    sh.init_cold()
+    sh.run(30, norms=False)
+    thr = np.array([0.0, 1e-6, -1e-6])
+    e, gap, smooth = sh.check(thr)
+    # the same shadow certified by one f64 handle from the assembled z
+    S = _native.GridSolver(g, precision="f64")
+    S.set_z(sh.assemble(sh.local_z()))
+    S.shadow()
+    e_ref, gap_ref, smooth_ref = S.check(thr)
+    scale = max(1.0, np.max(np.abs(e_ref)))
+    assert np.allclose(e, e_ref, rtol=0, atol=1e-6 * scale)
+    assert np.allclose(gap, gap_ref, rtol=0, atol=1e-6 * scale)
+    assert smooth == pytest.approx(smooth_ref, rel=1e-6)
+
+
+@pytest.mark.gpu
+def test_solve_sharded_certifies_integer_instance():
+    from paracut_b200 import _native
+    import paracut_b200 as pc
+    from paracut_b200.distributed import solve_sharded
+    g = make_instance(CONFIGS["cfg2_int"], seed=3, dims=(96, 80))
+    cfg = pc.SolverConfig(gap_tol=1e-6, max_iters=4000, check_every=20,
+                          thresholds=(0.0, 1e-6, -1e-6, 1e-3, -1e-3))
+    trace, k, gap, energy, ok = solve_sharded(
+        g, LocalComm(4), range(4), lambda sub: _native.GridSolver(sub, precision="f32"), cfg,
+        device="cuda")
+    ref = pc.solve(g, pc.decompose_grid(g), pc.SolverConfig(gap_tol=1e-6, max_iters=4000,
+                                                           check_every=20,
+                                                           thresholds=cfg.thresholds))
+    assert ok and ref.certified
+    assert energy == ref.energy  # integer instance: the same exact optimum
