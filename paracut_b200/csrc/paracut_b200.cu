@@ -783,7 +783,13 @@ struct pcb_solver {
   unsigned fmask = 0xfu;  // families swept by this handle (sharded runs split them)
   int nbk[MAXR]{};        // fp32 path: blocks per chain (intra-chain split), 1 = whole chains
   int lbk[MAXR]{};        // block length (positions)
-  DBuf<int> merge;        // merge points, max_j nbk[j] * C_j
+  DBuf<int> merge;        // merge points, family j at merge_off[j] (nbk[j] * C_j entries)
+  int64_t merge_off[MAXR]{};
+  // merges of a step run on a side stream, overlapping the sweeps (they
+  // depend only on the state at the start of the step)
+  bool overlap_merges = true;  // PCB_OVERLAP_MERGE=0 runs them inline
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_merge[MAXR] = {};
   // profiling: event pairs around family launches
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -791,6 +797,10 @@ struct pcb_solver {
   std::vector<int> ev_fam;
   ~pcb_solver() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (ev_start) cudaEventDestroy(ev_start);
+    for (cudaEvent_t e : ev_merge)
+      if (e) cudaEventDestroy(e);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -1118,23 +1128,37 @@ int launch_role(pcb_solver* h, const pcb::fast::Args& a, int j) {
                                : launch_sweep<ROLE, false>(h, a, h->maps[j]);
 }
 
-// merge points of family j for the current state (before its sweep)
-int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) {
+// merge points of family j for the current state (before its sweep), on
+// stream st; a.merge / a.nb point the sweep at them
+int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a, cudaStream_t st) {
   a.merge = nullptr;
   a.nb = 1;
   if (h->nbk[j] <= 1) return 0;
   const Fam& F = h->fam[j];
   const int per = pcb::fast::MWARPS * 32;
   const dim3 g((unsigned)((F.C + per - 1) / per), (unsigned)(h->nbk[j] - 1));
+  int* out = h->merge.p + h->merge_off[j];
   if (fam_rowlike(F.kind))
-    pcb::fast::k_merge<true><<<g, per, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
-                                                       4 * h->lbk[j], h->merge.p);
+    pcb::fast::k_merge<true><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+                                                4 * h->lbk[j], out);
   else
-    pcb::fast::k_merge<false><<<g, per, 0, h->stream>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
-                                                        4 * h->lbk[j], h->merge.p);
+    pcb::fast::k_merge<false><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+                                                 4 * h->lbk[j], out);
   LAUNCH_CHECK(h);
-  a.merge = h->merge.p;
+  a.merge = out;
   a.nb = h->nbk[j];
+  return 0;
+}
+
+int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) { return launch_merge(h, j, a, h->stream); }
+
+// side stream + events for the overlapped merges (created on first use)
+int ensure_side(pcb_solver* h) {
+  if (h->side) return 0;
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+  for (int j = 0; j < MAXR; ++j)
+    CUDA_TRY(cudaEventCreateWithFlags(&h->ev_merge[j], cudaEventDisableTiming));
   return 0;
 }
 
@@ -1235,6 +1259,27 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
   const bool noupd = flags & PCB_STEP_NO_UPDATE;
   if (na == 1 && !preset && !noupd) CUDA_TRY(cudaMemsetAsync(h->G32.p, 0, h->n * sizeof(float),
                                                               h->stream));
+  // Every merge depends only on the state at the start of the step (p_j, the
+  // drift c, the weights): launch them all on the side stream now, so they
+  // run in the earlier sweeps' tails; sweep j waits for merge j only.
+  bool side_merge[MAXR] = {};
+  if (h->overlap_merges) {
+    bool any = false;
+    for (int q = 0; q < na; ++q) any = any || h->nbk[act[q]] > 1;
+    if (any) {
+      if (int e = ensure_side(h)) return e;
+      CUDA_TRY(cudaEventRecord(h->ev_start, h->stream));
+      CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_start, 0));
+      for (int q = 0; q < na; ++q) {
+        const int j = act[q];
+        if (h->nbk[j] <= 1) continue;
+        pcb::fast::Args m{h->fam[j], h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p};
+        if (int rc = launch_merge(h, j, m, h->side)) return rc;
+        CUDA_TRY(cudaEventRecord(h->ev_merge[j], h->side));
+        side_merge[j] = true;
+      }
+    }
+  }
   int64_t off = 0;
   for (int q = 0; q < na; ++q) {
     const int j = act[q];
@@ -1246,8 +1291,14 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
                       h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
                       (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
+    int rc = 0;
+    if (side_merge[j]) {
+      CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_merge[j], 0));
+      a.merge = h->merge.p + h->merge_off[j];
+      a.nb = h->nbk[j];
+    }
     prof_begin(h, j);
-    int rc = launch_merge(h, j, a);
+    if (!side_merge[j]) rc = launch_merge(h, j, a);
     if (!rc) {
       if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a, j);
       else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a, j);
@@ -1308,10 +1359,13 @@ int choose_split(pcb_solver* h) {
     nb = (F.m + lb - 1) / lb;
     h->nbk[j] = nb;
     h->lbk[j] = lb;
-    if (nb > 1 && (int64_t)nb * F.C > need) need = (int64_t)nb * F.C;
+    h->merge_off[j] = need;
+    if (nb > 1) need += (int64_t)nb * F.C;
   }
   if (need > 0)
     if (int e = h->merge.alloc(need)) return e;
+  const char* ov = getenv("PCB_OVERLAP_MERGE");
+  h->overlap_merges = !(ov && ov[0] == '0');
   return 0;
 }
 
