@@ -35,6 +35,9 @@ using fast::cp_wait;
 // than SMs; 2D grids have only ~side chains per family) are bound by one
 // warp's own latency and want the deeper 32-position ring.  All families of
 // a sweep are independent (y_j depends on z_j only) and run in one launch.
+#ifndef PCB_EXACT_KEEP
+#define PCB_EXACT_KEEP 16  // a round ends when at most this many lanes still have data
+#endif
 constexpr int WARPS = 4;
 constexpr int TP = 8;   // positions per tile
 constexpr int HCX = 6;  // hull entries per lane in shared memory
@@ -420,7 +423,7 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
     for (;;) {
       const int lo_pos = t_lo * TP;
       const int avail_hi = min(t_rdy * TP, m);
-      scan(lo_pos, avail_hi, (t_rdy < t_ld) ? 16 : 0);
+      scan(lo_pos, avail_hi, (t_rdy < t_ld) ? PCB_EXACT_KEEP : 0);
       __syncwarp();
       if (__all_sync(0xffffffffu, done)) {
         cp_wait(0);
