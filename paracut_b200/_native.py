@@ -137,6 +137,31 @@ def debug_counters(reset=True):
     return out
 
 
+_HUGE_MIN = 32 << 20
+
+
+def _host_empty(shape, dtype=np.float64):
+    """Uninitialised host array for a large device read-back.
+
+    Backed by an anonymous mapping advised for transparent huge pages, so the
+    first-touch faults of the copy-out are 2 MB ones instead of 4 KB ones
+    (fresh np.empty memory faults at ~20 GB/s on the B200 hosts).  Small
+    arrays are plain np.empty.
+    """
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape)) * dt.itemsize
+    if nbytes < _HUGE_MIN:
+        return np.empty(shape, dtype=dt)
+    import mmap
+    mm = mmap.mmap(-1, nbytes, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+    if hasattr(mm, "madvise") and hasattr(mmap, "MADV_HUGEPAGE"):
+        try:
+            mm.madvise(mmap.MADV_HUGEPAGE)
+        except OSError:
+            pass
+    return np.frombuffer(mm, dtype=dt).reshape(shape)
+
+
 def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
@@ -210,7 +235,7 @@ class GridSolver:
         check(lib().pcb_set_z(self.handle, ptr(z)))
 
     def get_z(self):
-        z = np.empty((self.r, self.n))
+        z = _host_empty((self.r, self.n))
         check(lib().pcb_get_z(self.handle, ptr(z)))
         return z
 
@@ -238,13 +263,13 @@ class GridSolver:
         return int(p_.value), int(n_.value)
 
     def shadow(self, want_y=False, want_s=False):
-        y = np.empty((self.r, self.n)) if want_y else None
-        s = np.empty(self.n) if want_s else None
+        y = _host_empty((self.r, self.n)) if want_y else None
+        s = _host_empty((self.n,)) if want_s else None
         check(lib().pcb_shadow(self.handle, ptr(y), ptr(s)))
         return y, s
 
     def shadow_get(self):
-        y = np.empty((self.r, self.n))
+        y = _host_empty((self.r, self.n))
         check(lib().pcb_shadow_get(self.handle, ptr(y)))
         return y
 
@@ -272,7 +297,7 @@ class GridSolver:
         return lab
 
     def check_x(self, t=0):
-        x = np.empty(self.n)
+        x = _host_empty((self.n,))
         check(lib().pcb_get_check(self.handle, int(t), None, 0, ptr(x)))
         return x
 
@@ -280,8 +305,8 @@ class GridSolver:
         check(lib().pcb_keep_best(self.handle, int(t)))
 
     def get_best(self):
-        lab = np.empty(self.n, dtype=np.uint8)
-        x = np.empty(self.n)
+        lab = _host_empty((self.n,), np.uint8)
+        x = _host_empty((self.n,))
         check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
         return lab, x
 

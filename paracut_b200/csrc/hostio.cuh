@@ -14,9 +14,15 @@
 
 namespace hostio {
 
-constexpr size_t CHUNK = (size_t)16 << 20;
+#ifndef PCB_HOSTIO_CHUNK_MB
+#define PCB_HOSTIO_CHUNK_MB 16
+#endif
+#ifndef PCB_HOSTIO_THREADS
+#define PCB_HOSTIO_THREADS 8
+#endif
+constexpr size_t CHUNK = (size_t)PCB_HOSTIO_CHUNK_MB << 20;
 constexpr int SLOTS = 4;
-constexpr int THREADS = 8;
+constexpr int THREADS = PCB_HOSTIO_THREADS;
 constexpr size_t DIRECT_BELOW = (size_t)4 << 20;
 
 // Persistent worker threads that split one memcpy between them.
