@@ -87,6 +87,11 @@ int pcb_create(const int64_t *dims, int ndim, int conn, int precision, const dou
  * count, truncated header or payload). */
 int pcb_create_from_file(const char *path, int precision, int device, pcb_solver **out,
                          int64_t *dims_out, int *ndim_out, int *conn_out);
+/* Lambda path on a resident instance: every pairwise weight becomes
+ * factor * (its value at creation), as scaled_pairwise (graph.py:182-187), with
+ * the AAR state left in place -- the warm start of solve(g.scaled_pairwise(f),
+ * warm_start=previous, force_warm=True) without re-uploading the instance. */
+int pcb_scale_pairwise(pcb_solver *h, double factor);
 int pcb_destroy(pcb_solver *h);
 /* Device memory of destroyed handles stays mapped in a per-device pool for
  * the next handle; this returns it to the driver. */

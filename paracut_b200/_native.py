@@ -66,6 +66,7 @@ def _declare(L):
     L.pcb_level_set.argtypes = [P, P, P, P]
     L.pcb_dual_init.argtypes = [P, INT, P]
     L.pcb_release_memory.argtypes = [INT]
+    L.pcb_scale_pairwise.argtypes = [P, ctypes.c_double]
     L.pcb_create_from_file.argtypes = [ctypes.c_char_p, INT, INT, P, P, P, P]
     L.pcb_debug_counters.argtypes = [P, INT]
     L.pcb_dual_run.argtypes = [P, I64, P, P]
@@ -84,7 +85,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_synchronize", "pcb_init_cold", "pcb_set_z", "pcb_get_z", "pcb_aar_run",
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
-           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
+           "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count")
 
 
@@ -309,6 +310,10 @@ class GridSolver:
         x = _host_empty((self.n,))
         check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
         return lab, x
+
+    def scale_pairwise(self, factor):
+        """Pairwise weights := factor * creation weights; AAR state kept."""
+        check(lib().pcb_scale_pairwise(self.handle, float(factor)))
 
     def dual_init(self, alg, y0=None):
         """Start a BCD/AP/FISTA iterate (ALG_*) from y0 (r, n) or zeros."""

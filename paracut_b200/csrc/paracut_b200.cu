@@ -758,6 +758,7 @@ struct pcb_solver {
 
   DBuf<double> w;
   DBuf<double> dirw[4];
+  DBuf<double> dirw_base[4];  // lambda = 1 weights, kept on the first pcb_scale_pairwise
   DBuf<double> wf64[MAXR];
   DBuf<float> wf32[MAXR];
   DBuf<double> z;      // F64: r*n AAR point
@@ -956,6 +957,12 @@ int ensure_wf32(pcb_solver* h) {
     }
   }
   return 0;
+}
+
+__global__ void k_scale(const double* base, double* out, int64_t n, double f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = base[i] * f;  // graph.py:182-187: edge_a * factor
 }
 
 int ensure_spill(pcb_solver* h) {
@@ -1628,6 +1635,48 @@ int pcb_debug_counters(uint64_t* out, int reset) {
   (void)reset;
   for (int i = 0; i < 8; ++i) out[i] = 0;
 #endif
+  return 0;
+}
+
+int pcb_scale_pairwise(pcb_solver* h, double factor) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!(factor >= 0.0)) return fail(PCB_E_ARG, "scale factor must be nonnegative");
+  if (int e = set_dev(h)) return e;
+  DirPtrs dp{};
+  for (int k = 0; k < h->DG.ndir; ++k) {
+    const int64_t cnt = dir_size(h, k);
+    if (!h->dirw_base[k].p) {
+      if (int e = h->dirw_base[k].alloc(cnt)) return e;
+      if (cnt > 0)
+        CUDA_TRY(cudaMemcpyAsync(h->dirw_base[k].p, h->dirw[k].p, cnt * sizeof(double),
+                                 cudaMemcpyDeviceToDevice, h->stream));
+    }
+    if (cnt > 0) {
+      k_scale<<<grid_for(cnt, 256, NODE_GRID), 256, 0, h->stream>>>(h->dirw_base[k].p,
+                                                                     h->dirw[k].p, cnt, factor);
+      LAUNCH_CHECK(h);
+    }
+    dp.p[k] = h->dirw[k].p;
+  }
+  // family weights of both precisions from the rescaled direction arrays
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    const int64_t cnt = F.C * (int64_t)(F.m > 1 ? F.m - 1 : 0);
+    if (cnt == 0) continue;
+    if (h->wf64[j].p) {
+      k_build_family_weights<double><<<grid_for(cnt, 256, 148 * 16), 256, 0, h->stream>>>(
+          F, h->D, dp, h->wf64[j].p);
+      LAUNCH_CHECK(h);
+    }
+    if (h->wf32[j].p) {
+      k_build_family_weights<float><<<grid_for(cnt, 256, 148 * 16), 256, 0, h->stream>>>(
+          F, h->D, dp, h->wf32[j].p);
+      LAUNCH_CHECK(h);
+    }
+  }
+  h->have_shadow = false;
+  h->y_valid = false;
+  h->have_check = false;
   return 0;
 }
 

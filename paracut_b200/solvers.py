@@ -175,7 +175,7 @@ class _DeviceDualState(DualState):
 class _Driver:
     """Per-solve bookkeeping mirroring solvers.py:124-209."""
 
-    def __init__(self, g, dec, cfg):
+    def __init__(self, g, dec, cfg, solver=None):
         if not isinstance(dec, (GridDecomposition, ChainDecomposition)) or dec.n != g.n:
             raise ValueError("decomposition does not match the instance")
         if not isinstance(dec, GridDecomposition):
@@ -195,7 +195,8 @@ class _Driver:
         self.stopped = False
         self._labs = []
         self.thr = np.asarray(cfg.thresholds, dtype=np.float64)
-        self.solver = _native.GridSolver(g, precision=cfg.precision, device=cfg.device)
+        self.solver = (solver if solver is not None else
+                       _native.GridSolver(g, precision=cfg.precision, device=cfg.device))
         self.best_solver = None
         self.kmax = cfg.max_iters
         self.t0 = time.perf_counter()
@@ -293,11 +294,16 @@ class _Driver:
                            threshold=self.best_thr)
 
 
-def solve_aar(g, dec, cfg):
-    """Averaged alternating reflections on the device (solvers.py:272-307)."""
-    g = as_grid(g)
-    drv = _Driver(g, dec, cfg)
-    drv.warm_or_cold()
+def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
+    """Averaged alternating reflections on the device (solvers.py:272-307).
+
+    (_solver, _resident, _make64: used by solve_path to run on a resident
+    instance whose AAR state continues from the previous solve.)"""
+    if _solver is None:
+        g = as_grid(g)
+    drv = _Driver(g, dec, cfg, solver=_solver)
+    if not _resident:
+        drv.warm_or_cold()
     S = drv.solver
     k = 0
     if cfg.dual_tol > 0:
@@ -320,7 +326,8 @@ def solve_aar(g, dec, cfg):
     if cfg.precision == "f32" and cfg.polish_iters > 0 and not drv.stopped:
         # fp32 state leaves a ~1e-5 floor on the discrete gap of large instances;
         # continue in the exact fp64 mode from the same AAR point to certify
-        S64 = _native.GridSolver(g, precision="f64", device=cfg.device)
+        S64 = (_make64() if _make64 is not None else
+               _native.GridSolver(g, precision="f64", device=cfg.device))
         S64.set_z(S.get_z())
         drv.solver = S64
         drv.kmax = k + cfg.polish_iters
@@ -342,6 +349,85 @@ def _loop(drv, S, k):
             nxt = drv.next_due(k)
             drv.record("aar_step_norm", S.run(nxt - k))
             k = nxt
+
+
+class _ScaledGrid:
+    """g.scaled_pairwise(factor) without materialising it: structure for the
+    decomposition, weights and fingerprint computed on first use."""
+
+    def __init__(self, base, factor):
+        self._base, self._factor = base, float(factor)
+        self.dims, self.connectivity, self.n = tuple(base.dims), base.connectivity, base.n
+        self._grid = None
+
+    def _load(self):
+        if self._grid is None:
+            self._grid = self._base.scaled_pairwise(self._factor)
+        return self._grid
+
+    @property
+    def w(self):
+        return self._base.w
+
+    @property
+    def dir_weights(self):
+        return self._load().dir_weights
+
+    def tv(self, x):
+        return self._load().tv(x)
+
+    def energy(self, x):
+        return self._load().energy(x)
+
+    def _fingerprint(self):
+        return instance_fingerprint(self._load())
+
+
+def solve_path(g, lambdas, cfg, keep_states=True):
+    """Warm-started lambda path on one resident device instance.
+
+    Same results as the reference usage (SURVEY 8(d) cfg5)::
+
+        res = None
+        for lam in lambdas:
+            res = solve(g.scaled_pairwise(lam), dec,
+                        replace(cfg, warm_start=res and res.dual_state, force_warm=True))
+
+    but the instance is uploaded once: each step rescales the pairwise
+    weights on the device from the lambda = 1 copy (``pcb_scale_pairwise``)
+    and the AAR state simply continues (the warm start, bitwise in f64).
+    AAR only.  Returns the list of SolveResults; with ``keep_states=False``
+    only the last one carries a dual state (the others skip the read-back).
+    """
+    import dataclasses
+    if cfg.algorithm != "aar":
+        raise ValueError("solve_path runs the AAR scheme")
+    if cfg.dual_tol > 0:
+        raise ValueError("solve_path: dual_tol stopping is not supported")
+    g = as_grid(g)
+    S = _native.GridSolver(g, precision=cfg.precision, device=cfg.device)
+    out = []
+    for i, lam in enumerate(lambdas):
+        if lam < 0:
+            raise ValueError("scale factor must be nonnegative")
+        S.scale_pairwise(lam)
+        gl = _ScaledGrid(g, lam)
+        c = cfg if i == 0 else dataclasses.replace(cfg, warm_start=None, force_warm=True)
+
+        def make64(lam=lam):
+            T = _native.GridSolver(g, precision="f64", device=cfg.device)
+            T.scale_pairwise(lam)
+            return T
+        res = solve_aar(gl, GridDecomposition(gl), c, _solver=S, _resident=i > 0,
+                        _make64=make64)
+        if i + 1 < len(lambdas):  # the device state moves on: freeze this step's
+            if keep_states:
+                st = res.dual_state
+                res.dual_state = DualState(y=st.y, z=st.z, fingerprint=st.fingerprint)
+            else:
+                res.dual_state = None
+        out.append(res)
+    return out
 
 
 def _solve_dual(g, dec, cfg, alg, monitor_name):

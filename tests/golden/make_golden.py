@@ -221,6 +221,7 @@ def main():
     make_levels()
     make_dual()
     make_io()
+    make_path()
 
 
 def make_levels():
@@ -330,7 +331,38 @@ def make_io():
     print("wrote", out)
 
 
-if __name__ == "__main__" and "io" in sys.argv[1:]:
+def make_path():
+    """Warm-started lambda path the reference way (scaled_pairwise + force_warm)."""
+    global _PC
+    pc = import_reference()
+    _PC = pc
+    sys.path.insert(0, REPO)
+    from paracut_b200.instances import synth_image, energy_from_image
+    r = np.random.default_rng(41)
+    cases = [("r3d6", pc.random_grid((6, 5, 7), "3D-6", r))]
+    ours = energy_from_image(synth_image((40, 36), 4, 3, 9, seed=13), "2D-4", integer=True)
+    cases.append(("i2d4", pc.GridEnergy(ours.dims, "2D-4", ours.w, ours.dir_weights)))
+    lams = [0.25, 0.5, 1.0, 2.0]
+    for name, g in cases:
+        d = grid_arrays(g)
+        d["lambdas"] = np.array(lams)
+        res = None
+        for i, lam in enumerate(lams):
+            gl = g.scaled_pairwise(lam)
+            cfg = pc.SolverConfig(algorithm="aar", gap_tol=1e-6, max_iters=400, check_every=10,
+                                  warm_start=res.dual_state if res else None, force_warm=True)
+            res = pc.solve(gl, pc.decompose_grid(gl), cfg)
+            d.update({"iters_%d" % i: np.array(res.iterations), "energy_%d" % i: np.array(res.energy),
+                      "gap_%d" % i: np.array(res.gap), "certified_%d" % i: np.array(res.certified),
+                      "labeling_%d" % i: res.labeling, "y_%d" % i: res.dual_state.y,
+                      "z_%d" % i: res.dual_state.z,
+                      "fp_%d" % i: np.array(res.dual_state.fingerprint)})
+        save("path_%s.npz" % name, **d)
+
+
+if __name__ == "__main__" and "path" in sys.argv[1:]:
+    make_path()
+elif __name__ == "__main__" and "io" in sys.argv[1:]:
     make_io()
 elif __name__ == "__main__" and "levels" in sys.argv[1:]:
     make_levels()
