@@ -467,43 +467,145 @@ __global__ void k_get_fast(const float* p, const double* cdrift, double* z, int6
 }
 
 // Check-iteration update from the fp64 shadow y (state p^{k-1}, c^{k-1} -> p^k, c^k).
+// The fp32 state p_j sits in family layout [pos][chain]; for the row-like
+// families (pos = last grid coordinate) that is the transpose of node order,
+// so the grid is walked in 32 x 32 tiles (32 rows of the flattened leading
+// coordinates x 32 last-axis positions) and those families' p go through a
+// shared-memory tile: both the family-layout and the node-order accesses are
+// coalesced.  Per-node arithmetic is the same as a plain node loop.
+constexpr int APPLY_TILE = 32;
+constexpr int APPLY_THREADS = 256;  // launch with exactly this many threads
+
 template <int R>
-__global__ void k_apply_fast(const double* y, float* p, double* cdrift, float* X, const double* w,
-                             int64_t n, FamSet FS, Dims D, double* parts) {
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply_fast(
+    const double* __restrict__ y, float* __restrict__ p, double* __restrict__ cdrift,
+    float* __restrict__ X, const double* __restrict__ w, int64_t n,
+    const __grid_constant__ FamSet FS, const __grid_constant__ Dims D, double* parts) {
+  constexpr int T = APPLY_TILE, NW = APPLY_THREADS / 32;
+  constexpr int CELLS = (T + 1) * T, PASSES = (CELLS + APPLY_THREADS - 1) / APPLY_THREADS;
+  // chains R0-1 .. R0+T-1 (zig-zag chain c covers rows c and c+1) x T positions
+  __shared__ float tile[R][T + 1][T + 1];
+  const int64_t L = D.nd == 3 ? D.d[2] : D.d[1];
+  const int64_t rows = n / L;
+  const int64_t D1 = D.nd == 3 ? D.d[1] : 1;
+  const int64_t D0L = D.nd == 3 ? D.d[0] * L : 0;
+  const int64_t tiles_x = (L + T - 1) / T;
+  const int64_t tiles = ((rows + T - 1) / T) * tiles_x;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   double acc = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double g = 0.0, sp = 0.0;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t R0 = (t / tiles_x) * T;
+    const int64_t X0 = (t % tiles_x) * T;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
-      int64_t c;
-      int pos;
-      if (!fam_index(FS.f[j], D, i, &c, &pos)) continue;
-      const int64_t q = j * n + (int64_t)pos * FS.f[j].C + c;
-      const float pn = (float)y[j * n + i];
-      const double d = (double)pn - (double)p[q];
-      p[q] = pn;
-      g += d;
-      sp += (double)pn;
-      acc += d * d;
+      const Fam& F = FS.f[j];
+      if (!fam_rowlike(F.kind)) continue;
+      float v[PASSES];
+#pragma unroll
+      for (int k = 0; k < PASSES; ++k) {
+        const int e = threadIdx.x + k * APPLY_THREADS;
+        const int cc = e % (T + 1), xx = e / (T + 1);
+        const int64_t c = R0 - 1 + cc, x = X0 + xx;
+        v[k] = (e < CELLS && c >= 0 && c < F.C && x < L) ? p[j * n + x * F.C + c] : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < PASSES; ++k) {
+        const int e = threadIdx.x + k * APPLY_THREADS;
+        if (e < CELLS) tile[j][e % (T + 1)][e / (T + 1)] = v[k];
+      }
     }
-    const double xn = w[i] - sp;
-    X[i] = (float)xn;
-    const double dc = (xn - g) / (double)R;
-    cdrift[i] += dc;
-    acc += 2.0 * dc * g + (double)R * dc * dc;
+    __syncthreads();
+    // all loads of the warp's T/NW rows first (memory-level parallelism),
+    // then the arithmetic and the stores
+    // rows per batch: bounded so the register file holds two blocks per SM
+    constexpr int S = R >= 4 ? 2 : T / NW;
+#pragma unroll 1
+    for (int b0 = 0; b0 < T / NW; b0 += S) {
+    double yv[S][R], wv[S], cv[S];
+    float po[S][R];
+    int64_t qv[S][R];
+    bool in[S][R];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t Rr = R0 + wp + (b0 + s) * NW, x = X0 + lane;
+      const bool ok = Rr < rows && x < L;
+      const int64_t i = ok ? Rr * L + x : 0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const Fam& F = FS.f[j];
+        yv[s][j] = ok ? y[j * n + i] : 0.0;
+        if (fam_rowlike(F.kind)) {
+          const int64_t c = (F.kind == K_ZZ0 || F.kind == K_ZZ1) ? Rr - ((x + F.phase) & 1) : Rr;
+          in[s][j] = ok && c >= 0 && c < F.C;  // zig-zag border node: not in this family
+          qv[s][j] = c - (R0 - 1);              // tile row
+          po[s][j] = in[s][j] ? tile[j][qv[s][j]][lane] : 0.f;
+        } else {
+          // COL2 / Z3: family layout == node order; Y3: [y][z][x]
+          in[s][j] = ok;
+          qv[s][j] = j * n + (F.kind == K_Y3 ? (Rr % D1) * D0L + (Rr / D1) * L + x : i);
+          po[s][j] = ok ? p[qv[s][j]] : 0.f;
+        }
+      }
+      wv[s] = ok ? w[i] : 0.0;
+      cv[s] = ok ? cdrift[i] : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t Rr = R0 + wp + (b0 + s) * NW, x = X0 + lane;
+      if (Rr >= rows || x >= L) continue;
+      const int64_t i = Rr * L + x;
+      double g = 0.0, sp = 0.0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (!in[s][j]) continue;
+        const float pn = (float)yv[s][j];
+        if (fam_rowlike(FS.f[j].kind)) tile[j][qv[s][j]][lane] = pn;
+        else p[qv[s][j]] = pn;
+        const double d = (double)pn - (double)po[s][j];
+        g += d;
+        sp += (double)pn;
+        acc += d * d;
+      }
+      const double xn = wv[s] - sp;
+      X[i] = (float)xn;
+      const double dc = (xn - g) / (double)R;
+      cdrift[i] = cv[s] + dc;
+      acc += 2.0 * dc * g + (double)R * dc * dc;
+    }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const Fam& F = FS.f[j];
+      if (!fam_rowlike(F.kind)) continue;
+      const bool zz = F.kind == K_ZZ0 || F.kind == K_ZZ1;
+#pragma unroll
+      for (int k = 0; k < PASSES; ++k) {
+        const int e = threadIdx.x + k * APPLY_THREADS;
+        const int cc = e % (T + 1), xx = e / (T + 1);
+        const int64_t c = R0 - 1 + cc, x = X0 + xx;
+        const int64_t row = zz ? c + ((x + F.phase) & 1) : c;  // the node (c, x) sits in
+        if (e < CELLS && c >= 0 && c < F.C && x < L && row >= R0 && row < R0 + T && row < rows)
+          p[j * n + x * F.C + c] = tile[j][cc][xx];
+      }
+    }
+    __syncthreads();
   }
   __shared__ double sh[32];
-  const double t = block_sum(acc, sh);
-  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+  const double tot = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = tot;
 }
 
 // s = y_0 + y_1 + ... (class order), x = w - s, label bits per threshold,
 // partial sums: [unary_t (T)], dual, ww, dd.
 __global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n, int T,
                               const double* thr, uint8_t* bits, double* xcur, double* parts) {
-  double un[MAXT];
-  for (int t = 0; t < MAXT; ++t) un[t] = 0.0;
+  double un[MAXT], th[MAXT];  // register arrays: every index below is static
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    un[t] = 0.0;
+    th[t] = t < T ? thr[t] : 0.0;
+  }
   double dual = 0.0, ww = 0.0, dd = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -513,8 +615,9 @@ __global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n
     const double x = wi - s;
     xcur[i] = x;
     unsigned b = 0;
-    for (int t = 0; t < T; ++t) {
-      if (x > thr[t]) {
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t) {
+      if (t < T && x > th[t]) {
         b |= 1u << t;
         un[t] += wi;
       }
@@ -527,7 +630,9 @@ __global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n
   }
   __shared__ double sh[32];
   const int nv = T + 3;
-  for (int t = 0; t < T; ++t) {
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    if (t >= T) break;
     const double v = block_sum(un[t], sh);
     if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + t] = v;
   }
@@ -545,43 +650,66 @@ struct DirGeom {
 };
 
 // cut_t = sum_edges a_e |lab_t(i) - lab_t(j)|, per direction array element.
-__global__ void k_check_edges(Dims D, DirGeom DG, DirPtrs dw, const uint8_t* bits, int T,
+// One block walks whole grid rows (flattened leading coordinates); per row
+// and direction the edge-array row and the neighbour offset are computed
+// once, and the threads stride along the last axis (coalesced a_e and bits).
+__global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_constant__ DirGeom DG,
+                              const __grid_constant__ DirPtrs dw, const uint8_t* bits, int T,
                               double* parts) {
   double cut[MAXT];
+#pragma unroll
   for (int t = 0; t < MAXT; ++t) cut[t] = 0.0;
-  int64_t n = 1;
-  for (int a = 0; a < D.nd; ++a) n *= D.d[a];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t co[3];
-    int64_t rem = i;
-    for (int a = D.nd - 1; a >= 0; --a) {
-      co[a] = rem % D.d[a];
-      rem /= D.d[a];
+  const int nd = D.nd;
+  const int64_t L = nd == 3 ? D.d[2] : D.d[1];
+  const int64_t rows = nd == 3 ? D.d[0] * D.d[1] : D.d[0];
+  for (int64_t Rr = blockIdx.x; Rr < rows; Rr += gridDim.x) {
+    int64_t co[2] = {Rr, 0};
+    if (nd == 3) {
+      co[0] = Rr / D.d[1];
+      co[1] = Rr % D.d[1];
     }
-    const unsigned bi = bits[i];
+    const int64_t base = Rr * L;
     for (int k = 0; k < DG.ndir; ++k) {
-      // i is the "sa" end of a k-edge iff every coordinate stays in range
+      // this row holds the "sa" end of direction-k edges iff every leading
+      // coordinate stays in range
       bool ok = true;
-      int64_t e = 0, j = 0;
-      for (int a = 0; a < D.nd; ++a) {
+      int64_t erow = 0, joff = 0, stride = L;
+#pragma unroll
+      for (int a = 1; a >= 0; --a) {
+        if (a > nd - 2) continue;
+        joff += DG.off[k][a] * stride;
+        stride *= D.d[a];
+      }
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        if (a > nd - 2) continue;
         const int o = DG.off[k][a];
         const int64_t len = D.d[a] - (o < 0 ? -o : o);
-        const int64_t lo = o >= 0 ? 0 : -o;
-        const int64_t q = co[a] - lo;
+        const int64_t q = co[a] - (o >= 0 ? 0 : -o);
         if (q < 0 || q >= len) ok = false;
-        e = e * (len > 0 ? len : 1) + q;
-        j = j * D.d[a] + (co[a] + o);
+        erow = erow * (len > 0 ? len : 1) + q;
       }
       if (!ok) continue;
-      const double av = dw.p[k][e];
-      const unsigned diff = bi ^ (unsigned)bits[j];
-      for (int t = 0; t < T; ++t)
-        if ((diff >> t) & 1u) cut[t] += av;
+      const int oL = DG.off[k][nd - 1];
+      joff += oL;
+      const int64_t lenL = L - (oL < 0 ? -oL : oL), loL = oL >= 0 ? 0 : -oL;
+      const double* av = dw.p[k] + erow * lenL - loL;  // element (erow, x - loL)
+      const uint8_t* bn = bits + base + joff;
+      for (int64_t x = loL + threadIdx.x; x < loL + lenL; x += blockDim.x) {
+        const unsigned diff = (unsigned)bits[base + x] ^ (unsigned)bn[x];
+        if (diff) {
+          const double a = av[x];
+#pragma unroll
+          for (int t = 0; t < MAXT; ++t)
+            if ((diff >> t) & 1u) cut[t] += a;  // bits >= T are never set
+        }
+      }
     }
   }
   __shared__ double sh[32];
-  for (int t = 0; t < T; ++t) {
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t) {
+    if (t >= T) break;
     const double v = block_sum(cut[t], sh);
     if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * T + t] = v;
   }

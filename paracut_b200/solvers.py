@@ -61,6 +61,8 @@ class SolverConfig:
     thresholds: tuple = (0.0,)
     device: int = 0
     polish_iters: int = 0   # f32 runs that end uncertified: up to this many f64 iterations
+    polish_stall: int = 0   # f32: start the polish early once the best gap has not halved
+                            # over this many checks (0: only at max_iters)
     level_sets: bool = False  # each check also tries the best level set of x (on the device)
 
     def __post_init__(self):
@@ -74,8 +76,8 @@ class SolverConfig:
             raise ValueError("threads and check_every must be >= 1")
         if self.precision not in PRECISIONS:
             raise ValueError("precision must be one of %r" % (PRECISIONS,))
-        if self.polish_iters < 0:
-            raise ValueError("polish_iters must be >= 0")
+        if self.polish_iters < 0 or self.polish_stall < 0:
+            raise ValueError("polish_iters and polish_stall must be >= 0")
         thr = tuple(float(t) for t in self.thresholds)
         if not 1 <= len(thr) <= MAX_THRESHOLDS:
             raise ValueError("1..%d thresholds supported" % MAX_THRESHOLDS)
@@ -199,6 +201,8 @@ class _Driver:
                        _native.GridSolver(g, precision=cfg.precision, device=cfg.device))
         self.best_solver = None
         self.kmax = cfg.max_iters
+        self.stall = 0  # > 0: leave the loop once the best gap stalls for this many checks
+        self._best_hist = []
         self.t0 = time.perf_counter()
 
     def warm_or_cold(self):
@@ -253,7 +257,13 @@ class _Driver:
         self.iterations = k
         if gap <= self.cfg.gap_tol + GAP_SLACK:
             self.stopped = True
+        self._best_hist.append(self.best_gap)
         return self.stopped
+
+    def stalled(self):
+        """The best gap has not halved over the last `stall` checks."""
+        h, w = self._best_hist, self.stall
+        return w > 0 and len(h) > w and not h[-1] <= 0.5 * h[-1 - w]
 
     def due(self, k):
         return k % self.cfg.check_every == 0 or k >= self.kmax
@@ -322,8 +332,12 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
                 break
             have_prev = True
         return drv.finish()
+    polish = cfg.precision == "f32" and cfg.polish_iters > 0
+    if polish:
+        drv.stall = cfg.polish_stall
     k = _loop(drv, S, k)
-    if cfg.precision == "f32" and cfg.polish_iters > 0 and not drv.stopped:
+    drv.stall = 0
+    if polish and not drv.stopped:
         # fp32 state leaves a ~1e-5 floor on the discrete gap of large instances;
         # continue in the exact fp64 mode from the same AAR point to certify
         S64 = (_make64() if _make64 is not None else
@@ -341,7 +355,7 @@ def _loop(drv, S, k):
     while True:
         if drv.due(k):
             S.shadow()
-            if drv.check(k) or k >= drv.kmax:
+            if drv.check(k) or k >= drv.kmax or drv.stalled():
                 return k
             drv.record("aar_step_norm", S.apply())
             k += 1

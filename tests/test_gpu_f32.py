@@ -161,3 +161,19 @@ def test_integer_full_size_f32_reaches_exact_optimum_and_polish_certifies():
     assert r32.certified
     assert r32.energy == r64.energy
     assert g.energy(r32.labeling) == r64.energy
+
+
+def test_stall_triggered_polish_certifies_before_max_iters():
+    """polish_stall: once the fp32 gap stops halving, the fp64 polish starts
+    early and certifies the same integer optimum (cfg2 integer variant)."""
+    g = make_instance(CONFIGS["cfg2_int"], seed=0)
+    thr = (0.0, 1e-6, -1e-6, 1e-3)
+    r64 = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=1000, check_every=10, thresholds=thr))
+    assert r64.certified
+    r32 = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=4000, check_every=10, precision="f32",
+                                   thresholds=thr, polish_iters=1000, polish_stall=10))
+    assert r32.certified and r32.energy == r64.energy
+    start = r32.monitor["polish_start"][0]
+    assert start < 4000 and r32.iterations < 1500

@@ -47,3 +47,13 @@ def test_random_instances_both_paths(monkeypatch, oracle_lib, seed):
     x = g.w - r32.dual_state.y.sum(axis=0)
     scale = max(float(np.max(np.abs(x_ref))), 1.0)
     assert float(np.max(np.abs(x - x_ref))) <= 1e-4 * scale, (g.connectivity, g.dims, k)
+    # checks every few iterations: the check-iteration update (tiled apply)
+    # runs on non-zero states of every family layout
+    ce = int(rng.integers(1, 5))
+    r32c = pc.solve(g, dec, pc.SolverConfig(max_iters=k, check_every=ce, precision="f32"))
+    if r32c.iterations != k:  # certified at an earlier check
+        _, y_ref, _ = oracle_lib.aar(g, r32c.iterations, threads=4)
+        x_ref = g.w - y_ref.sum(axis=0)
+        scale = max(float(np.max(np.abs(x_ref))), 1.0)
+    xc = g.w - r32c.dual_state.y.sum(axis=0)
+    assert float(np.max(np.abs(xc - x_ref))) <= 1e-4 * scale, (g.connectivity, g.dims, k, ce)

@@ -95,6 +95,8 @@ def test_solver_config_validation():
         pc.SolverConfig(precision="f16")
     with pytest.raises(ValueError, match="thresholds"):
         pc.SolverConfig(thresholds=tuple(range(9)))
+    with pytest.raises(ValueError, match="polish"):
+        pc.SolverConfig(polish_stall=-1)
     assert pc.SolverConfig().thresholds == (0.0,)
 
 
