@@ -45,6 +45,10 @@ typedef struct pcb_solver pcb_solver;
 const char *pcb_last_error(void);
 int pcb_version(void);
 int pcb_device_count(int *count);
+/* Host helper (no device work): Jaccard distance 1 - |A & B| / |A | B| of two
+ * np.packbits-packed labelings of nbytes bytes (0 when both are empty), the
+ * trace column certify.py:68-78 / solvers.py:200-203 fill at finish. */
+int pcb_jaccard_packed(const uint8_t *a, const uint8_t *b, int64_t nbytes, double *out);
 
 /* ---- operator level ------------------------------------------------------
  * Replaces _kernels.prox_chains(node_idx, chain_ptr, edge_w, c_lo, c_hi, v,

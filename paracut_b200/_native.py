@@ -74,6 +74,7 @@ def _declare(L):
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
     L.pcb_set_profiling.argtypes = [P, INT]
     L.pcb_profile_read.argtypes = [P, P, P]
+    L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
     L.pcb_launch_count.argtypes = [P]
     L.pcb_launch_count.restype = I64
     L.pcb_reset_launch_count.argtypes = [P]
@@ -86,7 +87,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
-           "pcb_reset_launch_count")
+           "pcb_reset_launch_count", "pcb_jaccard_packed")
 
 
 def lib():
@@ -139,6 +140,17 @@ def debug_counters(reset=True):
 
 
 _HUGE_MIN = 32 << 20
+
+
+def jaccard_packed(pa, pb):
+    """1 - |A & B| / |A | B| of two packbits labelings (host popcount in the library)."""
+    pa = np.ascontiguousarray(pa, dtype=np.uint8)
+    pb = np.ascontiguousarray(pb, dtype=np.uint8)
+    if pa.shape != pb.shape:
+        raise ValueError("packed labelings differ in length")
+    out = ctypes.c_double()
+    check(lib().pcb_jaccard_packed(ptr(pa), ptr(pb), pa.size, ctypes.byref(out)))
+    return out.value
 
 
 def _host_empty(shape, dtype=np.float64):

@@ -1527,6 +1527,27 @@ const char* pcb_last_error(void) { return g_err.c_str(); }
 
 int pcb_version(void) { return PCB_VERSION; }
 
+__attribute__((target("popcnt")))  // hardware POPCNT (x86-64 hosts of this image)
+int pcb_jaccard_packed(const uint8_t* a, const uint8_t* b, int64_t nbytes, double* out) {
+  if ((!a || !b) && nbytes > 0) return fail(PCB_E_ARG, "null argument");
+  if (!out || nbytes < 0) return fail(PCB_E_ARG, "bad argument");
+  uint64_t inter = 0, uni = 0;
+  int64_t i = 0;
+  for (; i + 8 <= nbytes; i += 8) {
+    uint64_t x, y;
+    memcpy(&x, a + i, 8);
+    memcpy(&y, b + i, 8);
+    inter += (uint64_t)__builtin_popcountll(x & y);
+    uni += (uint64_t)__builtin_popcountll(x | y);
+  }
+  for (; i < nbytes; ++i) {
+    inter += (uint64_t)__builtin_popcount((unsigned)(a[i] & b[i]));
+    uni += (uint64_t)__builtin_popcount((unsigned)(a[i] | b[i]));
+  }
+  *out = uni == 0 ? 0.0 : 1.0 - (double)inter / (double)uni;
+  return 0;
+}
+
 int pcb_device_count(int* count) {
   if (!count) return fail(PCB_E_ARG, "count is null");
   CUDA_TRY(cudaGetDeviceCount(count));

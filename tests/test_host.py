@@ -110,10 +110,15 @@ def test_threshold_and_level_sets():
 def test_jaccard_packed_equals_unpacked():
     from paracut_b200.certify import jaccard_packed
     rng = np.random.default_rng(0)
-    for n in (1, 7, 8, 9, 1000):
+    from paracut_b200 import _native
+    for n in (1, 7, 8, 9, 63, 64, 65, 1000, 100003):
         a = (rng.random(n) < 0.4).astype(np.uint8)
         b = (rng.random(n) < 0.6).astype(np.uint8)
-        assert jaccard_packed(np.packbits(a), np.packbits(b)) == pc.jaccard_distance(a, b)
+        ref = pc.jaccard_distance(a, b)
+        assert jaccard_packed(np.packbits(a), np.packbits(b)) == ref
+        assert _native.jaccard_packed(np.packbits(a), np.packbits(b)) == ref  # host popcount
+    z = np.zeros(5, np.uint8)
+    assert _native.jaccard_packed(z, z) == 0.0 == pc.jaccard_distance(z, z)
 
 
 def test_generator_reproduces_cfg1_fixture():
