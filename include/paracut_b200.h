@@ -132,14 +132,23 @@ int pcb_aar_step(pcb_solver *h, int64_t iters, int flags, double *step_norms);
 /* Sweep only families whose bit is set (decompose_grid order). */
 int pcb_set_family_mask(pcb_solver *h, unsigned mask);
 /* x -= g; c += (x - g)/r on this handle's nodes, g a device pointer to n
- * floats (the exported g of the slab side, already in this handle's layout). */
+ * floats (the exported g of the slab side, already in this handle's layout).
+ * The LAST role's step-norm term sum(2 dc g + r dc^2) over the owned nodes
+ * lands in norms[1] (PCB_BUF_NORMS). */
 int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
+/* Nodes [n_own, n) of this handle are halo copies of nodes another shard
+ * owns (2D-8 row slabs carry the next slab's first row for the zig-zag path
+ * that straddles the boundary): pcb_check labels them (their edges to owned
+ * nodes are this shard's) but leaves their unary / dual terms to the owner,
+ * and pcb_apply_g leaves their norm term out.  n_own = n: no halo. */
+int pcb_set_owned(pcb_solver *h, int64_t n_own);
 /* Device pointer and element count of a handle buffer (for collectives). */
 #define PCB_BUF_G 0      /* float[n] accumulator / exported g */
 #define PCB_BUF_X 1      /* float[n] primal                  */
 #define PCB_BUF_C 2      /* double[n] drift                  */
 #define PCB_BUF_Y 3      /* double[r*n] shadow               */
 #define PCB_BUF_NORMS 4  /* double[] per-iteration norms      */
+#define PCB_BUF_P 5      /* float[r*n] fp32 family state (family layout) */
 int pcb_device_buffer(pcb_solver *h, int which, uintptr_t *ptr, int64_t *count);
 
 /* Shadow y = Pi_K(z) into the handle's shadow buffer (projections.py:89-104);

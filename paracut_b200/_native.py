@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
 
 PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
-BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
+BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_P = 0, 1, 2, 3, 4, 5
 ALG_BCD, ALG_AP, ALG_FISTA = 1, 2, 3
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
 PRECISIONS = {"f64": 0, "f32": 1}
@@ -75,6 +75,7 @@ def _declare(L):
     L.pcb_set_profiling.argtypes = [P, INT]
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
+    L.pcb_set_owned.argtypes = [P, I64]
     L.pcb_launch_count.argtypes = [P]
     L.pcb_launch_count.restype = I64
     L.pcb_reset_launch_count.argtypes = [P]
@@ -87,7 +88,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
-           "pcb_reset_launch_count", "pcb_jaccard_packed")
+           "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned")
 
 
 def lib():
@@ -268,6 +269,10 @@ class GridSolver:
 
     def apply_g(self, g_dev_ptr):
         check(lib().pcb_apply_g(self.handle, int(g_dev_ptr)))
+
+    def set_owned(self, n_own):
+        """Nodes [n_own, n) are halo copies owned by another shard (pcb_set_owned)."""
+        check(lib().pcb_set_owned(self.handle, int(n_own)))
 
     def device_buffer(self, which):
         """(device pointer, element count) of a handle buffer (BUF_*)."""

@@ -426,9 +426,18 @@ __global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, 
   const int r = FS.r;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    // z_j = p_j + c.  A zig-zag border node keeps no state in that family
+    // (p = 0), so there c = its z; elsewhere c = mean_j z_j.  (States the
+    // solver produces have z equal across the border families of a node.)
     double m = 0.0;
-    for (int j = 0; j < r; ++j) m += z[j * n + i];
-    m /= (double)r;
+    int border = -1;
+    for (int j = 0; j < r; ++j) {
+      int64_t c;
+      int pos;
+      m += z[j * n + i];
+      if (border < 0 && !fam_index(FS.f[j], D, i, &c, &pos)) border = j;
+    }
+    m = border >= 0 ? z[border * n + i] : m / (double)r;
     double sp = 0.0;
     for (int j = 0; j < r; ++j) {
       int64_t c;
@@ -598,8 +607,9 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fast(
 
 // s = y_0 + y_1 + ... (class order), x = w - s, label bits per threshold,
 // partial sums: [unary_t (T)], dual, ww, dd.
-__global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n, int T,
-                              const double* thr, uint8_t* bits, double* xcur, double* parts) {
+__global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n, int64_t n_own,
+                              int T, const double* thr, uint8_t* bits, double* xcur,
+                              double* parts) {
   double un[MAXT], th[MAXT];  // register arrays: every index below is static
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
@@ -614,15 +624,17 @@ __global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n
     const double wi = w[i];
     const double x = wi - s;
     xcur[i] = x;
+    const bool own = i < n_own;  // halo copies: labels for the cut, sums are the owner's
     unsigned b = 0;
 #pragma unroll
     for (int t = 0; t < MAXT; ++t) {
       if (t < T && x > th[t]) {
         b |= 1u << t;
-        un[t] += wi;
+        if (own) un[t] += wi;
       }
     }
     bits[i] = (uint8_t)b;
+    if (!own) continue;
     const double sw = s - wi;
     dual += fmin(sw, 0.0);
     ww += wi * wi;
@@ -870,6 +882,7 @@ struct pcb_solver {
   DirGeom DG{};
   int r = 0;
   int64_t n = 0;
+  int64_t n_own = -1;  // nodes [n_own, n) are halo copies (pcb_set_owned); -1: none
   Fam fam[MAXR]{};
   int order[MAXR]{};  // fast-mode processing order (last one covers all nodes)
   int maxm = 1;
@@ -1451,14 +1464,21 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
 
 // x -= g; c += (x - g) / r on this handle's nodes (the pencil copy of the
 // drift in a sharded run), with g exported by the slab side's LAST family
-__global__ void k_apply_g(const float* g, float* X, double* cdr, int64_t n, double inv_r) {
+__global__ void k_apply_g(const float* g, float* X, double* cdr, int64_t n, int64_t n_own,
+                          double inv_r, double rd, double* parts) {
+  double acc = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double gv = (double)g[i];
     const double xn = (double)X[i] - gv;
     X[i] = (float)xn;
-    cdr[i] += (xn - gv) * inv_r;
+    const double dcv = (xn - gv) * inv_r;
+    cdr[i] += dcv;
+    if (i < n_own) acc += 2.0 * dcv * gv + rd * dcv * dcv;  // the LAST role's norm term
   }
+  __shared__ double sh[32];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
 }
 
 int shadow_fast(pcb_solver* h) {
@@ -1694,7 +1714,7 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   if ((rc = h->xcur.alloc(n))) return bail(rc);
   if ((rc = h->parts.alloc(parts_needed(h)))) return bail(rc);
   if ((rc = h->vals.alloc(64))) return bail(rc);
-  if ((rc = h->norms.alloc(1))) return bail(rc);
+  if ((rc = h->norms.alloc(2))) return bail(rc);
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "setup: %s", cudaGetErrorString(e)));
   phase("rest");
@@ -2048,7 +2068,9 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
   CUDA_TRY(hostio::h2d(h->vals.p + 48, thr, nthr * sizeof(double), h->stream));
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   const int nv = nthr + 3;
-  k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n, nthr, h->vals.p + 48,
+  k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n,
+                                                 h->n_own < 0 ? h->n : h->n_own, nthr,
+                                                 h->vals.p + 48,
                                                  h->bits.p, h->xcur.p, h->parts.p);
   LAUNCH_CHECK(h);
   k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nv, h->vals.p);
@@ -2303,9 +2325,22 @@ int pcb_apply_g(pcb_solver* h, uintptr_t g_dev) {
   if (!h || !g_dev) return fail(PCB_E_ARG, "null argument");
   if (h->precision != PCB_F32) return fail(PCB_E_ARG, "apply_g needs the f32 path");
   if (int e = set_dev(h)) return e;
-  k_apply_g<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
-      reinterpret_cast<const float*>(g_dev), h->X32.p, h->cdrift.p, h->n, 1.0 / (double)h->r);
+  const int g = grid_for(h->n, 256, NODE_GRID);
+  k_apply_g<<<g, 256, 0, h->stream>>>(reinterpret_cast<const float*>(g_dev), h->X32.p,
+                                      h->cdrift.p, h->n, h->n_own < 0 ? h->n : h->n_own,
+                                      1.0 / (double)h->r, (double)h->r, h->parts.p);
   LAUNCH_CHECK(h);
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p + 1, 0);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+int pcb_set_owned(pcb_solver* h, int64_t n_own) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (n_own < 0 || n_own > h->n) return fail(PCB_E_ARG, "owned node count %lld out of [0, %lld]",
+                                             (long long)n_own, (long long)h->n);
+  h->n_own = n_own == h->n ? -1 : n_own;
+  h->have_check = false;
   return 0;
 }
 
@@ -2317,6 +2352,7 @@ int pcb_device_buffer(pcb_solver* h, int which, uintptr_t* ptr, int64_t* count) 
     case PCB_BUF_C: *ptr = (uintptr_t)h->cdrift.p; *count = h->cdrift.p ? h->n : 0; break;
     case PCB_BUF_Y: *ptr = (uintptr_t)h->y.p; *count = (int64_t)h->r * h->n; break;
     case PCB_BUF_NORMS: *ptr = (uintptr_t)h->norms.p; *count = (int64_t)h->norms.n; break;
+    case PCB_BUF_P: *ptr = (uintptr_t)h->p32.p; *count = h->p32.p ? (int64_t)h->r * h->n : 0; break;
     default: return fail(PCB_E_ARG, "unknown buffer id %d", which);
   }
   if (!*ptr) return fail(PCB_E_STATE, "buffer %d not allocated for this precision", which);

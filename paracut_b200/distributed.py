@@ -14,7 +14,17 @@ One iteration (the fused (p_j, c) form of solvers.py:295-298):
     pencil : x -= g; c += (x - g)/r   (pencil copy of the drift)
 
 so each iteration moves 2 * 4 bytes per node across ranks (both bounded
-quantities; the divergent drift c never travels).  Step norms are reduced
+quantities; the divergent drift c never travels).
+
+2D-8 row slabs: rows and zig-zag pairs inside a slab are local, the zig-zag
+path of the pair straddling a boundary runs on the upper rank, whose handle
+carries the next slab's first row as a halo (``SlabGeometry.halo``).  Its
+iteration replaces the slab's LAST role by ``apply_g`` after two one-row
+exchanges (the path's d up to the owner, the owner's complete g back down),
+so the owner's and the halo's drift and primal stay bitwise equal; the
+certificate moves the path's shadow up and the owner's full first-row shadow
+down, and the halo's unary / dual terms are left to the owner
+(``pcb_set_owned``).  Step norms are reduced
 across ranks as partial sums of squares.  Communication goes through a
 ``comm`` object (``TorchComm`` over torch.distributed -- NCCL on GPUs, gloo
 on CPU -- or ``LocalComm`` for P virtual ranks in one process), so the
@@ -34,8 +44,15 @@ import numpy as np
 
 from .graph import DIRECTIONS, GridEnergy, as_grid
 
-CROSS = {"2D-4": 1, "3D-6": 2}          # family that crosses slabs
-LOCAL = {"2D-4": (0,), "3D-6": (0, 1)}  # families inside a slab
+CROSS = {"2D-4": 1, "2D-8": 1, "3D-6": 2}                # family that crosses slabs
+LOCAL = {"2D-4": (0,), "2D-8": (0, 2, 3), "3D-6": (0, 1)}  # families inside a slab
+# 2D-8: the zig-zag path of the row pair that straddles a slab boundary is
+# swept by the upper slab's rank, whose handle carries the next slab's first
+# row as a halo (row-direction weights zeroed there, so that row's row chains
+# are inert singletons); the path's d / shadow on the halo row move to the
+# owner and the owner's complete g / shadow come back.
+HALO = {"2D-8"}
+ZIGZAG_PHASE = {2: 0, 3: 1}  # 2D-8 family -> phase: node (row, x) of pair row - ((x + phase) & 1)
 
 
 class SlabGeometry:
@@ -43,7 +60,8 @@ class SlabGeometry:
 
     def __init__(self, dims, connectivity, world):
         if connectivity not in CROSS:
-            raise ValueError("slab sharding supports 2D-4 and 3D-6 grids, not %r" % connectivity)
+            raise ValueError("slab sharding supports 2D-4, 2D-8 and 3D-6 grids, not %r"
+                             % connectivity)
         self.dims = tuple(int(d) for d in dims)
         self.conn = connectivity
         self.P = int(world)
@@ -57,8 +75,14 @@ class SlabGeometry:
         self.n_slab = self.dz * self.plane
         self.n_pencil = D0 * self.cp
 
+    def halo(self, rank):
+        """Rows of the next slab this rank's handle carries (2D-8: 1, except the last rank)."""
+        return 1 if self.conn in HALO and rank < self.P - 1 else 0
+
     def slab_grid(self, g, rank):
         """GridEnergy of rank's slab (all directions sliced; the cross one is unused)."""
+        if self.conn in HALO:
+            return self._halo_slab_grid(g, rank)
         z0, z1 = rank * self.dz, (rank + 1) * self.dz
         dims = (self.dz,) + self.dims[1:]
         w = g.w.reshape(self.dims)[z0:z1].ravel()
@@ -70,6 +94,22 @@ class SlabGeometry:
         k = CROSS[self.conn]
         dws[k] = np.ascontiguousarray(g.dir_weights[k][z0:z0 + max(self.dz - 1, 0)])
         return GridEnergy(dims, self.conn, np.ascontiguousarray(w), dws)
+
+    def _halo_slab_grid(self, g, rank):
+        """2D-8 row slab plus the next slab's first row: rows and zig-zag pairs
+        of the slab, the straddling pair, and the column edges to the halo row
+        (the slab's certificate counts them); the halo row's row edges are 0."""
+        z0, h = rank * self.dz, self.dz + self.halo(rank)
+        W = self.dims[1]
+        w = np.ascontiguousarray(g.w.reshape(self.dims)[z0:z0 + h].ravel())
+        rows = np.array(g.dir_weights[0][z0:z0 + h], dtype=np.float64)
+        if self.halo(rank):
+            rows[-1] = 0.0
+        cols = np.ascontiguousarray(g.dir_weights[1][z0:z0 + h - 1])
+        d1 = np.ascontiguousarray(g.dir_weights[2][z0:z0 + h - 1])
+        d2 = np.ascontiguousarray(g.dir_weights[3][z0:z0 + h - 1])
+        assert rows.shape == (h, W - 1) and cols.shape == (h - 1, W)
+        return GridEnergy((h, W), self.conn, w, [rows, cols, d1, d2])
 
     def pencil_cols(self, rank):
         return np.arange(rank * self.cp, (rank + 1) * self.cp)
@@ -88,6 +128,8 @@ class SlabGeometry:
         else:
             dims = (D0, self.cp)
             dws = [np.zeros((D0, self.cp - 1)), a.reshape(D0 - 1, self.cp)]
+            if self.conn == "2D-8":
+                dws += [np.zeros((D0 - 1, self.cp - 1)), np.zeros((D0 - 1, self.cp - 1))]
         return GridEnergy(dims, self.conn, np.ascontiguousarray(w.ravel()),
                           [np.ascontiguousarray(x) for x in dws])
 
@@ -103,6 +145,16 @@ class LocalComm:
         for r in range(self.world):
             for q in range(self.world):
                 recvs[r][q].copy_(sends[q][r])
+
+    def send_next(self, sends, recvs):
+        """recvs[r] <- sends[r - 1] (sends[P-1] and recvs[0] are None)."""
+        for r in range(1, self.world):
+            recvs[r].copy_(sends[r - 1])
+
+    def send_prev(self, sends, recvs):
+        """recvs[r] <- sends[r + 1] (sends[0] and recvs[P-1] are None)."""
+        for r in range(self.world - 1):
+            recvs[r].copy_(sends[r + 1])
 
     def all_sum(self, values):
         tot = np.zeros_like(np.asarray(values[0], dtype=np.float64))
@@ -123,6 +175,24 @@ class TorchComm:
     def all_to_all(self, sends, recvs):
         (s,), (r,) = sends, recvs
         self.dist.all_to_all_single(r.view(-1), s.reshape(-1).contiguous())
+
+    def _p2p(self, send, send_to, recv, recv_from):
+        ops = []
+        if send is not None:
+            ops.append(self.dist.P2POp(self.dist.isend, send.contiguous(), send_to))
+        if recv is not None:
+            ops.append(self.dist.P2POp(self.dist.irecv, recv, recv_from))
+        if ops:
+            for req in self.dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def send_next(self, sends, recvs):
+        (s,), (r,) = sends, recvs
+        self._p2p(s, self.rank + 1, r, self.rank - 1)
+
+    def send_prev(self, sends, recvs):
+        (s,), (r,) = sends, recvs
+        self._p2p(s, self.rank - 1, r, self.rank + 1)
 
     def all_sum(self, values):
         import torch
@@ -173,13 +243,19 @@ class ShardedAAR:
         self.r = len(DIRECTIONS[g.connectivity])
         self.cross = CROSS[g.connectivity]
         self.slab, self.pencil = [], []
+        self.halo = g.connectivity in HALO
         for rk in self.ranks:
             s = backend(self.geo.slab_grid(g, rk))
             p = backend(self.geo.pencil_grid(g, rk))
             s.set_family_mask(sum(1 << j for j in LOCAL[g.connectivity]))
             p.set_family_mask(1 << self.cross)
+            if self.geo.halo(rk):
+                s.set_owned(self.geo.n_slab)
             self.slab.append(s)
             self.pencil.append(p)
+        W = self.geo.dims[-1]
+        # zig-zag nodes of an owner's first row that lie on the straddling path
+        self._straddle = {j: (np.arange(W) + ph) % 2 == 1 for j, ph in ZIGZAG_PHASE.items()}
         self.device = device
         self._bufs = []
         for s, p in zip(self.slab, self.pencil):
@@ -190,6 +266,11 @@ class ShardedAAR:
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
         self._recv_s = [torch.empty((P, dz, cp), dtype=torch.float32, device=self._dev())
                         for _ in self.ranks]
+        if self.halo:
+            self._hrow = [torch.empty(W, dtype=torch.float32, device=self._dev())
+                          for _ in self.ranks]
+            self._mask = {j: torch.as_tensor(m, device=self._dev())
+                          for j, m in self._straddle.items()}
 
     def _dev(self):
         return self.device if self.device is not None else "cpu"
@@ -211,10 +292,74 @@ class ShardedAAR:
         """Warm start from a global AAR point z (r, n), natural layout."""
         z = np.asarray(z, dtype=np.float64).reshape(self.r, self.g.dims[0], self.geo.plane)
         for i, rk in enumerate(self.ranks):
-            z0, z1 = rk * self.geo.dz, (rk + 1) * self.geo.dz
-            self.slab[i].set_z(np.ascontiguousarray(z[:, z0:z1].reshape(self.r, -1)))
+            z0, z1 = rk * self.geo.dz, (rk + 1) * self.geo.dz + self.geo.halo(rk)
+            zs = np.ascontiguousarray(z[:, z0:z1])
+            emu = hasattr(self.slab[i], "host_buffer")
+            if self.halo and not emu:
+                fix = self._halo_seam_z(z, zs, rk)
+            self.slab[i].set_z(zs.reshape(self.r, -1))
+            if self.halo:
+                self._zero_halo_rows(i, rk)
+                if not emu:
+                    self._set_seam_x(i, fix)
             cols = self.geo.pencil_cols(rk)
             self.pencil[i].set_z(np.ascontiguousarray(z[:, :, cols].reshape(self.r, -1)))
+
+    def _halo_seam_z(self, z, zs, rk):
+        """On the seam rows (an owner's first row, a halo row) each slab handle
+        lacks one zig-zag family that the global grid has there, and its
+        set_z takes the drift from that border family.  Hand it the global
+        drift (mean over families, the single handle's choice for these
+        interior nodes); returns {local row: global primal X} to restore."""
+        dz, W = self.geo.dz, self.geo.dims[-1]
+        fix = {}
+        seams = ([(0, True)] if rk > 0 else []) + ([(dz, False)] if self.geo.halo(rk) else [])
+        for row, on_path in seams:
+            zg = z[:, rk * dz + row]
+            m = zg[0].copy()
+            for j in range(1, self.r):
+                m = m + zg[j]
+            m = m / self.r
+            for j, msk in self._straddle.items():
+                lack = msk if on_path else ~msk  # nodes whose family-j state is elsewhere
+                zs[j, row, lack] = m[lack]
+            sp = np.zeros(W)
+            for j in range(self.r):
+                sp = sp + (zg[j] - m).astype(np.float32).astype(np.float64)
+            w = self.g.w.reshape(self.g.dims)[rk * dz + row]
+            fix[row] = (w - sp).astype(np.float32)
+        return fix
+
+    def _set_seam_x(self, i, fix):
+        import torch
+        W = self.geo.dims[-1]
+        X = self._tensor(self.slab[i], self.N.BUF_X, np.float32)
+        for row, x in fix.items():
+            X[row * W:(row + 1) * W] = torch.as_tensor(x, device=self._dev())
+
+    def _zero_halo_rows(self, i, rk):
+        """The halo row's row chains are inert: their state stays 0 (its drift
+        and primal keep the owner's values)."""
+        h, ns, W = self.slab[i], self.geo.n_slab, self.geo.dims[-1]
+        if hasattr(h, "host_buffer"):
+            # CPU emulation keeps node-order state for every family, where the
+            # device keeps none for zig-zag border nodes: zero what another
+            # rank's path owns (halo row off the straddling path, the owner's
+            # first row on it)
+            if self.geo.halo(rk):
+                h.p[0][ns:] = 0
+                for j, m in self._straddle.items():
+                    h.p[j][ns:][~m] = 0
+            if rk > 0:
+                for j, m in self._straddle.items():
+                    h.p[j][:W][m] = 0
+            return
+        if not self.geo.halo(rk):
+            return
+        ptr, cnt = h.device_buffer(self.N.BUF_P)
+        rows = ns // W + 1
+        # family 0 (rows) in family layout [pos = x][chain = row]
+        _wrap(ptr, cnt, np.float32, self._dev())[:rows * W].view(W, rows)[:, rows - 1].zero_()
 
     # ---------------------------------------------------------------- iterations
     def run(self, iters, norms=True):
@@ -227,7 +372,9 @@ class ShardedAAR:
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
         K = int(iters)
         acc = [torch.zeros(K, dtype=torch.float64, device=self._dev()) for _ in self.ranks]
-        for k in range(K):
+        if self.halo:
+            self._run_halo(K, acc)
+        for k in range(0 if self.halo else K):
             for i, p in enumerate(self.pencil):
                 p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
                 acc[i][k] += self._bufs[i]["Np"][0]
@@ -253,6 +400,48 @@ class ShardedAAR:
         tot = self.comm.all_sum([a.cpu().numpy() for a in acc])
         return np.sqrt(np.maximum(np.asarray(tot[0], dtype=np.float64), 0.0))
 
+    def _run_halo(self, K, acc):
+        """2D-8 iterations: every slab-side update goes through apply_g once the
+        halo row's g is complete, so the owner's and the halo's copies of the
+        drift and primal stay bitwise equal."""
+        N = self.N
+        P, dz, cp, ns, W = self.geo.P, self.geo.dz, self.geo.cp, self.geo.n_slab, self.geo.dims[-1]
+        first = [rk > 0 for rk in self.ranks]
+        has_halo = [bool(self.geo.halo(rk)) for rk in self.ranks]
+        for k in range(K):
+            for i, p in enumerate(self.pencil):
+                p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
+                acc[i][k] += self._bufs[i]["Np"][0]
+            sends = [b["Gp"].view(P, dz, cp) for b in self._bufs]
+            self.comm.all_to_all(sends, self._recv_s)
+            for i, b in enumerate(self._bufs):
+                b["Gs"][:ns].view(dz, P, cp).copy_(self._recv_s[i].transpose(0, 1))
+                b["Gs"][ns:].zero_()
+            for i, s in enumerate(self.slab):
+                s.step(1, N.STEP_G_PRESET | N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
+                acc[i][k] += self._bufs[i]["Ns"][0]
+            # halo up: the straddling paths' d on the halo row -> the owner's first row
+            self.comm.send_next([b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)],
+                                [hr if f else None for hr, f in zip(self._hrow, first)])
+            for i, b in enumerate(self._bufs):
+                if first[i]:
+                    b["Gs"][:W] += self._hrow[i]
+            # slab -> pencil: the complete g of the owned rows
+            sends = [b["Gs"][:ns].view(dz, P, cp).transpose(0, 1).contiguous() for b in self._bufs]
+            recvs = [b["Gp"].view(P, dz, cp) for b in self._bufs]
+            self.comm.all_to_all(sends, recvs)
+            # halo down: the owner's complete g of its first row -> the halo row
+            self.comm.send_prev([b["Gs"][:W] if f else None for b, f in zip(self._bufs, first)],
+                                [b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)])
+            for i, (s, p) in enumerate(zip(self.slab, self.pencil)):
+                if hasattr(s, "host_buffer"):
+                    s.apply_g_host(self._bufs[i]["Gs"].numpy())
+                    p.apply_g_host(self._bufs[i]["Gp"].numpy())
+                else:
+                    s.apply_g(self._bufs[i]["Gs"].data_ptr())
+                    p.apply_g(self._bufs[i]["Gp"].data_ptr())
+                acc[i][k] += self._bufs[i]["Ns"][1]
+
     # ---------------------------------------------------------------- certificates
     def _ybuf(self, h):
         if hasattr(h, "host_buffer"):  # CPU emulation
@@ -273,34 +462,68 @@ class ShardedAAR:
         for s, p in zip(self.slab, self.pencil):
             s.shadow()
             p.shadow()
+        # slab handles hold ns (+ one halo row) nodes per family
+        next_ = [ns + plane * self.geo.halo(rk) for rk in self.ranks]
+        ys = [self._ybuf(s).view(self.r, ne) for s, ne in zip(self.slab, next_)]
         # the cross family's shadow: pencil (D0, cp) -> slab (dz, P * cp)
         sends = [self._ybuf(p)[x * npn:(x + 1) * npn].view(P, dz, cp) for p in self.pencil]
         recvs = [torch.empty((P, dz, cp), dtype=torch.float64, device=self._dev())
                  for _ in self.ranks]
         self.comm.all_to_all(sends, recvs)
-        for s, rv in zip(self.slab, recvs):
-            self._ybuf(s)[x * ns:(x + 1) * ns].view(dz, P, cp).copy_(rv.transpose(0, 1))
+        for y, rv in zip(ys, recvs):
+            y[x, :ns].view(dz, P, cp).copy_(rv.transpose(0, 1))
+        if self.halo:
+            self._halo_shadow(ys)
         # per-rank certificate of the slab (its nodes, its intra-slab edges)
         a_b = np.asarray(self.g.dir_weights[x], dtype=np.float64).reshape(self.g.dims[0] - 1, plane)
         firsts_local, local = [], []
         for rk, s in zip(self.ranks, self.slab):
             e, gp, smooth = s.check(thr)
-            labs = np.stack([s.check_labels(t) for t in range(T)]).astype(np.float64)
-            mine = np.zeros((P, T, plane))
-            mine[rk] = labs[:, :plane]  # this slab's first label plane, for rank rk - 1
-            firsts_local.append(mine)
-            local.append((rk, e, float(e[0] - gp[0]), float(smooth), labs[:, -plane:]))
-        firsts = self.comm.all_sum(firsts_local)[0]
+            last = None
+            if not self.halo:
+                labs = np.stack([s.check_labels(t) for t in range(T)]).astype(np.float64)
+                mine = np.zeros((P, T, plane))
+                mine[rk] = labs[:, :plane]  # this slab's first label plane, for rank rk - 1
+                firsts_local.append(mine)
+                last = labs[:, -plane:]
+            local.append((rk, e, float(e[0] - gp[0]), float(smooth), last))
+        firsts = None if self.halo else self.comm.all_sum(firsts_local)[0]
         parts = []
         for rk, e, dual, smooth, last in local:
             cut_b = np.zeros(T)
-            if rk < P - 1:  # edges between this slab's last plane and the next one's first
+            # edges between this slab's last plane and the next one's first
+            # (2D-8: already in the slab's certificate through the halo row)
+            if rk < P - 1 and not self.halo:
                 cut_b = np.abs(last - firsts[rk + 1]) @ a_b[(rk + 1) * dz - 1]
             parts.append(np.concatenate([np.asarray(e, dtype=np.float64) + cut_b,
                                          [dual, smooth]]))
         tot = self.comm.all_sum(parts)[0]
         energies, dual, smooth = tot[:T], tot[T], tot[T + 1]
         return energies, energies - dual, smooth
+
+    def _halo_shadow(self, ys):
+        """2D-8: the straddling paths' shadow on a halo row joins the owner's
+        first row; then the owner's complete first-row shadow (all families)
+        becomes the halo row, so the halo's x and labels are the owner's."""
+        import torch
+        ns, W = self.geo.n_slab, self.geo.dims[-1]
+        zz = list(ZIGZAG_PHASE)
+        first = [rk > 0 for rk in self.ranks]
+        has_halo = [bool(self.geo.halo(rk)) for rk in self.ranks]
+        up = [torch.empty((len(zz), W), dtype=torch.float64, device=self._dev()) for _ in ys]
+        self.comm.send_next([y[zz, ns:ns + W].contiguous() if h else None
+                             for y, h in zip(ys, has_halo)],
+                            [u if f else None for u, f in zip(up, first)])
+        for y, u, f in zip(ys, up, first):
+            if f:
+                for t, j in enumerate(zz):
+                    y[j, :W] = torch.where(self._mask[j], u[t], y[j, :W])
+        down = [torch.empty((self.r, W), dtype=torch.float64, device=self._dev()) for _ in ys]
+        self.comm.send_prev([y[:, :W].contiguous() if f else None for y, f in zip(ys, first)],
+                            [d if h else None for d, h in zip(down, has_halo)])
+        for y, d, h in zip(ys, down, has_halo):
+            if h:
+                y[:, ns:ns + W] = d
 
     def capture(self):
         """Record one fused iteration (norms off) as a CUDA graph; replay it with
@@ -348,11 +571,23 @@ class ShardedAAR:
         D0, plane = self.g.dims[0], self.geo.plane
         out = np.zeros((self.r, D0, plane))
         loc = LOCAL[self.g.connectivity]
+        ns = self.geo.n_slab
         for rk, (sl, pe) in parts.items():
             z0, z1 = rk * self.geo.dz, (rk + 1) * self.geo.dz
             for t, j in enumerate(loc):
-                out[j, z0:z1] = sl[t].reshape(self.geo.dz, plane)
+                out[j, z0:z1] = sl[t][:ns].reshape(self.geo.dz, plane)
             out[self.cross][:, self.geo.pencil_cols(rk)] = pe.reshape(D0, self.geo.cp)
+        if self.g.connectivity in HALO:
+            # the straddling paths' nodes of each first row live on the rank above
+            W = self.g.dims[-1]
+            for rk, (sl, _) in parts.items():
+                if not self.geo.halo(rk):
+                    continue
+                z1 = (rk + 1) * self.geo.dz
+                for t, j in enumerate(loc):
+                    if j in ZIGZAG_PHASE:
+                        m = (np.arange(W) + ZIGZAG_PHASE[j]) % 2 == 1
+                        out[j, z1, m] = sl[t][ns:ns + W][m]
         return out.reshape(self.r, -1)
 
 

@@ -12,7 +12,7 @@ from oracle import oracle as orc
 
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
 BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
-ORDER = {"2D-4": (0, 1), "3D-6": (0, 1, 2)}
+ORDER = {"2D-4": (0, 1), "2D-8": (0, 1, 2, 3), "3D-6": (0, 1, 2)}
 
 
 class EmuSolver:
@@ -27,7 +27,8 @@ class EmuSolver:
         self.c = np.zeros(self.n)
         self.X = np.zeros(self.n, np.float32)
         self.G = np.zeros(self.n, np.float32)
-        self.norms = np.zeros(1)
+        self.norms = np.zeros(2)
+        self.n_own = self.n
         self.y = np.zeros((self.r, self.n))
         self.bits = None
 
@@ -37,6 +38,9 @@ class EmuSolver:
 
     def set_family_mask(self, mask):
         self.mask = mask
+
+    def set_owned(self, n_own):
+        self.n_own = int(n_own)
 
     def init_cold(self):
         self.p[:] = 0
@@ -108,7 +112,10 @@ class EmuSolver:
         gd = np.asarray(g, dtype=np.float32).astype(np.float64)
         xn = self.X.astype(np.float64) - gd
         self.X[:] = xn.astype(np.float32)
-        self.c += (xn - gd) / self.r
+        dcv = (xn - gd) * (1.0 / self.r)
+        self.c += dcv
+        o = self.n_own
+        self.norms[1] = float(np.sum(2.0 * dcv[:o] * gd[:o] + self.r * dcv[:o] * dcv[:o]))
 
     def shadow(self, want_y=True, want_s=False):
         for j in range(self.r):
@@ -123,10 +130,11 @@ class EmuSolver:
         x = self.w - s
         labs = (x[None, :] > np.asarray(thr)[:, None]).astype(np.uint8)
         self.bits = labs
-        e = np.array([orc.grid_tv(self.g, lab) - float(self.w @ lab) for lab in labs])
-        d = s - self.w
+        o = self.n_own  # halo nodes: labelled for the cut, their sums are the owner's
+        e = np.array([orc.grid_tv(self.g, lab) - float(self.w[:o] @ lab[:o]) for lab in labs])
+        d = (s - self.w)[:o]
         dual = float(np.minimum(d, 0.0).sum())
-        smooth = 0.5 * float(self.w @ self.w) - 0.5 * float(d @ d)
+        smooth = 0.5 * float(self.w[:o] @ self.w[:o]) - 0.5 * float(d @ d)
         return e, e - dual, smooth
 
     def check_labels(self, t, packed=False):

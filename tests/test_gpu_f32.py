@@ -177,3 +177,16 @@ def test_stall_triggered_polish_certifies_before_max_iters():
     assert r32.certified and r32.energy == r64.energy
     start = r32.monitor["polish_start"][0]
     assert start < 4000 and r32.iterations < 1500
+
+
+def test_f32_warm_start_keeps_zigzag_border_nodes():
+    """An AAR point of the exact path (2D-8) loads into the fp32 state and
+    reads back unchanged, zig-zag border nodes included (their z is the
+    drift: the fused state keeps no p there)."""
+    from paracut_b200 import _native
+    g = make_instance(CONFIGS["cfg3"], seed=2, dims=(40, 56))
+    r64 = pc.solve(g, pc.decompose_grid(g), pc.SolverConfig(max_iters=30, check_every=31))
+    z = r64.dual_state.z
+    S = _native.GridSolver(g, precision="f32")
+    S.set_z(z)
+    assert np.max(np.abs(S.get_z() - z)) <= 1e-6 * np.max(np.abs(z))
