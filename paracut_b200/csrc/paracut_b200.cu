@@ -1254,7 +1254,10 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
 
 template <int ROLE, bool ROWLIKE>
 int launch_sweep(pcb_solver* h, const pcb::fast::Args& a, const pcb::fast::Maps& M) {
-  const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>();
+#ifndef PCB_RING_PAD
+#define PCB_RING_PAD 0  // experiment knob: extra dynamic smem per block (occupancy probes)
+#endif
+  const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>() + PCB_RING_PAD;
   // set once per device (outside any later CUDA-graph capture of the sweep)
   static unsigned set_mask = 0;
   const unsigned bit = 1u << (h->device & 31);

@@ -16,6 +16,19 @@ One iteration (the fused (p_j, c) form of solvers.py:295-298):
 so each iteration moves 2 * 4 bytes per node across ranks (both bounded
 quantities; the divergent drift c never travels).
 
+Overlapped schedule (``overlap=True``, the default on GPUs for 3D-6 and
+2D-4): the slab sweeps do not wait for the cross family.  Two streams per
+process -- S (slab compute) and C (pencil compute + NCCL):
+
+    C: pencil sweep (FIRST, no update) -> d_z ; A2A #1           (record A)
+    S: slab sweeps (FIRST x, MID y, no update) -> G_s = d_x + d_y
+    S: wait A ; G_s += d_z ; apply_g (x, c, norm) ; pack g         (record J)
+    C: wait J ; A2A #2 ; pencil apply_g
+
+so A2A #1 and the pencil sweep run under the slab sweeps, and A2A #2 plus
+the pencil update of iteration k run under the slab sweeps of k + 1.  The
+per-node sum is d_x + d_y + d_z, the family order of the unsharded run.
+
 2D-8 row slabs: rows and zig-zag pairs inside a slab are local, the zig-zag
 path of the pair straddling a boundary runs on the upper rank, whose handle
 carries the next slab's first row as a halo (``SlabGeometry.halo``).  Its
@@ -231,7 +244,7 @@ class ShardedAAR:
     emulation in tests).
     """
 
-    def __init__(self, g, comm, ranks, backend, device=None):
+    def __init__(self, g, comm, ranks, backend, device=None, overlap=None):
         import torch
         from . import _native as N
         self.N = N
@@ -257,6 +270,8 @@ class ShardedAAR:
         # zig-zag nodes of an owner's first row that lie on the straddling path
         self._straddle = {j: (np.arange(W) + ph) % 2 == 1 for j, ph in ZIGZAG_PHASE.items()}
         self.device = device
+        # overlapped schedule (module docstring); 2D-8's halo exchanges keep the serial one
+        self.overlap = (not self.halo) if overlap is None else (bool(overlap) and not self.halo)
         self._bufs = []
         for s, p in zip(self.slab, self.pencil):
             self._bufs.append(dict(Gs=self._tensor(s, N.BUF_G, np.float32),
@@ -266,6 +281,10 @@ class ShardedAAR:
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
         self._recv_s = [torch.empty((P, dz, cp), dtype=torch.float32, device=self._dev())
                         for _ in self.ranks]
+        if self.overlap:  # packed g (slab -> pencil), separate from G_s so S can run ahead
+            self._send_g = [torch.empty((P, dz, cp), dtype=torch.float32, device=self._dev())
+                            for _ in self.ranks]
+            self._streams = None
         if self.halo:
             self._hrow = [torch.empty(W, dtype=torch.float32, device=self._dev())
                           for _ in self.ranks]
@@ -374,7 +393,9 @@ class ShardedAAR:
         acc = [torch.zeros(K, dtype=torch.float64, device=self._dev()) for _ in self.ranks]
         if self.halo:
             self._run_halo(K, acc)
-        for k in range(0 if self.halo else K):
+        elif self.overlap:
+            self._run_overlap(K, acc)
+        for k in range(0 if (self.halo or self.overlap) else K):
             for i, p in enumerate(self.pencil):
                 p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
                 acc[i][k] += self._bufs[i]["Np"][0]
@@ -399,6 +420,91 @@ class ShardedAAR:
             return None
         tot = self.comm.all_sum([a.cpu().numpy() for a in acc])
         return np.sqrt(np.maximum(np.asarray(tot[0], dtype=np.float64), 0.0))
+
+    def _stream_pair(self):
+        """(S, C) CUDA streams of the overlapped schedule, or (None, None) on CPU."""
+        import torch
+        if not (self.device is not None and str(self.device).startswith("cuda")):
+            return None, None
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(), torch.cuda.Stream())
+        return self._streams
+
+    def _run_overlap(self, K, acc):
+        """Overlapped iterations (module docstring): slab work on stream S, pencil
+        sweep / update and both all-to-alls on stream C, joined by two events per
+        iteration.  Forks from and joins back to the caller's current stream, so
+        it runs eagerly and inside a CUDA-graph capture alike."""
+        import contextlib
+        import torch
+        N = self.N
+        P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
+        S, C = self._stream_pair()
+        cuda = S is not None
+
+        def on(st):
+            return torch.cuda.stream(st) if cuda else contextlib.nullcontext()
+
+        acc_p = [torch.zeros_like(a) for a in acc]  # C-side partials (acc is S-side)
+        if cuda:
+            base = torch.cuda.current_stream()
+            S.wait_stream(base)
+            C.wait_stream(base)
+            for s in self.slab:
+                s.set_stream(S.cuda_stream)
+            for p in self.pencil:
+                p.set_stream(C.cuda_stream)
+        try:
+            for k in range(K):
+                with on(C):  # cross family: d_z, then pencil -> slab
+                    for i, p in enumerate(self.pencil):
+                        p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
+                        acc_p[i][k] += self._bufs[i]["Np"][0]
+                    self.comm.all_to_all([b["Gp"].view(P, dz, cp) for b in self._bufs],
+                                         self._recv_s)
+                    ev_a = torch.cuda.Event() if cuda else None
+                    if cuda:
+                        ev_a.record(C)
+                with on(S):  # local families while d_z is in flight
+                    for i, s in enumerate(self.slab):
+                        s.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
+                        acc[i][k] += self._bufs[i]["Ns"][0]
+                    if cuda:
+                        S.wait_event(ev_a)
+                    for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
+                        b["Gs"].view(dz, P, cp).add_(self._recv_s[i].transpose(0, 1))
+                        if hasattr(s, "host_buffer"):
+                            s.apply_g_host(b["Gs"].numpy())
+                        else:
+                            s.apply_g(b["Gs"].data_ptr())
+                        acc[i][k] += b["Ns"][1]
+                        self._send_g[i].copy_(b["Gs"].view(dz, P, cp).transpose(0, 1))
+                    ev_j = torch.cuda.Event() if cuda else None
+                    if cuda:
+                        ev_j.record(S)
+                with on(C):  # slab -> pencil g, pencil update (under the next slab sweeps)
+                    if cuda:
+                        C.wait_event(ev_j)
+                    recvs = [b["Gp"].view(P, dz, cp) for b in self._bufs]
+                    self.comm.all_to_all(self._send_g, recvs)
+                    for i, p in enumerate(self.pencil):
+                        if hasattr(p, "host_buffer"):
+                            p.apply_g_host(self._bufs[i]["Gp"].numpy())
+                        else:
+                            p.apply_g(self._bufs[i]["Gp"].data_ptr())
+        finally:
+            if cuda:
+                base.wait_stream(S)
+                base.wait_stream(C)
+                for h in self.slab + self.pencil:
+                    h.set_stream(base.cuda_stream)
+        if cuda:
+            with torch.cuda.stream(base):
+                for a, b in zip(acc, acc_p):
+                    a += b
+        else:
+            for a, b in zip(acc, acc_p):
+                a += b
 
     def _run_halo(self, K, acc):
         """2D-8 iterations: every slab-side update goes through apply_g once the

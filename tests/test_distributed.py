@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, conn, dims, iters, q):
+def _worker(rank, world, port, conn, dims, iters, q, overlap=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
     import torch.distributed as dist
@@ -32,7 +32,7 @@ def _worker(rank, world, port, conn, dims, iters, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = make_instance(SPEC[conn], seed=2, dims=dims)
-        sh = ShardedAAR(g, TorchComm(), [rank], EmuSolver)
+        sh = ShardedAAR(g, TorchComm(), [rank], EmuSolver, overlap=overlap)
         sh.init_cold()
         norms = sh.run(iters)
         parts = sh.local_z()
@@ -43,16 +43,17 @@ def _worker(rank, world, port, conn, dims, iters, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("conn,dims", [("3D-6", (6, 8, 5)), ("2D-4", (12, 10)),
-                                       ("2D-8", (12, 10))])
-def test_gloo_world2_matches_unsharded(conn, dims):
+@pytest.mark.parametrize("conn,dims,overlap", [("3D-6", (6, 8, 5), False), ("2D-4", (12, 10), False),
+                                               ("2D-8", (12, 10), False), ("3D-6", (6, 8, 5), True),
+                                               ("2D-4", (12, 10), True)])
+def test_gloo_world2_matches_unsharded(conn, dims, overlap):
     import multiprocessing as mp
     from emu import EmuSolver
     iters = 6
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, conn, dims, iters, q))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, conn, dims, iters, q, overlap))
              for r in range(2)]
     for p in procs:
         p.start()
@@ -64,11 +65,16 @@ def test_gloo_world2_matches_unsharded(conn, dims):
     ref = EmuSolver(g)
     ref.init_cold()
     # unsharded reference in the same family order as the sharded run:
-    # cross family first (FIRST), local families after, LAST = last local one
+    # serial schedule: cross family first (FIRST), local families after, LAST =
+    # last local one; overlapped schedule: local families first, cross last
+    # (the natural order)
     from emu import ORDER
     cross = {"2D-4": 1, "2D-8": 1, "3D-6": 2}[conn]
     ORDER_SAVE = ORDER[conn]
-    ORDER[conn] = (cross,) + tuple(j for j in ORDER_SAVE if j != cross)
+    if overlap:
+        ORDER[conn] = tuple(j for j in ORDER_SAVE if j != cross) + (cross,)
+    else:
+        ORDER[conn] = (cross,) + tuple(j for j in ORDER_SAVE if j != cross)
     try:
         ref_norms = ref.run(iters)
     finally:
@@ -91,7 +97,10 @@ def test_gloo_world2_matches_unsharded(conn, dims):
     # 2D-8: the straddling path's d joins the owner's fp32 accumulator after
     # the owner's own families (a different fp32 summation order), so the
     # iterates agree to fp32 rounding instead of exactly
-    tol = 1e-6 if conn == "2D-8" else 1e-9
+    # the overlapped schedule adds the cross family's d to the local
+    # families' fp32 sum after it was rounded to fp32 for the exchange (the
+    # unsharded LAST role adds it unrounded): fp32-rounding agreement too
+    tol = 1e-6 if (conn == "2D-8" or overlap) else 1e-9
     assert np.max(np.abs(z - z_ref)) <= tol * scale
     assert np.max(np.abs(y - y_ref)) <= tol * max(1.0, np.max(np.abs(y_ref)))
     for _, _, _, norms, _ in res:
@@ -133,18 +142,22 @@ def test_geometry_partition():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("P", [2, 4])
 @pytest.mark.parametrize("conn,dims", [("3D-6", (32, 24, 40)), ("2D-4", (64, 96)),
                                        ("2D-8", (64, 96))])
-def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims):
+def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims, overlap):
     """P slab/pencil handle pairs on one device (LocalComm, no kernel waits on
     another) reproduce the single-handle f32 run."""
     import paracut_b200 as pc
     from paracut_b200 import _native
     g = make_instance(SPEC[conn], seed=4, dims=dims)
     k = 25
+    if conn == "2D-8" and not overlap:
+        pytest.skip("2D-8 always runs the serial halo schedule")
     sh = ShardedAAR(g, LocalComm(P), range(P),
-                    lambda sub: _native.GridSolver(sub, precision="f32"), device="cuda")
+                    lambda sub: _native.GridSolver(sub, precision="f32"), device="cuda",
+                    overlap=overlap)
     sh.init_cold()
     norms = sh.run(k)
     z = sh.assemble(sh.local_z())
@@ -162,7 +175,8 @@ def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("conn,dims", [("3D-6", (16, 20, 24)), ("2D-8", (32, 48))])
+@pytest.mark.parametrize("conn,dims", [("3D-6", (16, 20, 24)), ("2D-4", (40, 56)),
+                                       ("2D-8", (32, 48))])
 def test_nccl_world1_and_graph_capture_match_eager(conn, dims):
     """The TorchComm/NCCL code path (world 1 in-process) and a CUDA-graph
     capture of one iteration give the same iterates as LocalComm eager."""
