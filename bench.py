@@ -54,6 +54,8 @@ def parse_args():
     ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--precision", default=None, choices=(None, "f32", "f64"))
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the slab-sharded NCCL path even at world size 1 (test of the N>1 path)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttc", action="store_true", help="skip the time-to-optimal-cut solves")
@@ -214,6 +216,8 @@ def run_sharded(args, world, rank, local):
     from paracut_b200.instances import CONFIGS, make_instance, algorithmic_bytes
 
     torch.cuda.set_device(local)
+    if "MASTER_ADDR" not in os.environ:  # --sharded without torchrun: world of one
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = CONFIGS[args.workload]
     g = make_instance(spec, seed=args.seed)
@@ -234,9 +238,6 @@ def run_sharded(args, world, rank, local):
     dist.barrier()
     torch.cuda.synchronize()
     handles = sh.slab + sh.pencil
-    for h in handles:
-        h.reset_launch_count()
-        h.set_profiling(True)
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
@@ -256,8 +257,20 @@ def run_sharded(args, world, rank, local):
     clocks.mark_end()
     ms = ev0.elapsed_time(ev1)
     clk = clocks.stop()
+    # graph replays carry no per-launch events: time the family kernels (and
+    # count this library's launches per iteration) over a few eager iterations
+    torch.cuda.synchronize()
+    for h in handles:
+        h.set_stream(0)
+        h.reset_launch_count()
+        h.set_profiling(True)
+    n_prof = 3
+    sh.run(n_prof, norms=False)
+    torch.cuda.synchronize()
     prof = [h.profile_read() for h in handles]
-    launches = sum(h.launch_count() for h in handles)
+    launches = sum(h.launch_count() for h in handles) * args.steps // n_prof
+    for h in handles:
+        h.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -324,7 +337,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
-    if world > 1:
+    if world > 1 or args.sharded:
         run_sharded(args, world, rank, local)
         return
 

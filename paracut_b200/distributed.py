@@ -28,6 +28,9 @@ process -- S (slab compute) and C (pencil compute + NCCL):
 so A2A #1 and the pencil sweep run under the slab sweeps, and A2A #2 plus
 the pencil update of iteration k run under the slab sweeps of k + 1.  The
 per-node sum is d_x + d_y + d_z, the family order of the unsharded run.
+2D-8 adds its two one-row halo exchanges on S: the straddling paths' d goes
+up before the cross family's d is added, the owner's complete first-row g
+comes back down before the slab update.
 
 2D-8 row slabs: rows and zig-zag pairs inside a slab are local, the zig-zag
 path of the pair straddling a boundary runs on the upper rank, whose handle
@@ -270,8 +273,8 @@ class ShardedAAR:
         # zig-zag nodes of an owner's first row that lie on the straddling path
         self._straddle = {j: (np.arange(W) + ph) % 2 == 1 for j, ph in ZIGZAG_PHASE.items()}
         self.device = device
-        # overlapped schedule (module docstring); 2D-8's halo exchanges keep the serial one
-        self.overlap = (not self.halo) if overlap is None else (bool(overlap) and not self.halo)
+        # overlapped schedule (module docstring)
+        self.overlap = True if overlap is None else bool(overlap)
         self._bufs = []
         for s, p in zip(self.slab, self.pencil):
             self._bufs.append(dict(Gs=self._tensor(s, N.BUF_G, np.float32),
@@ -391,10 +394,10 @@ class ShardedAAR:
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
         K = int(iters)
         acc = [torch.zeros(K, dtype=torch.float64, device=self._dev()) for _ in self.ranks]
-        if self.halo:
-            self._run_halo(K, acc)
-        elif self.overlap:
+        if self.overlap:
             self._run_overlap(K, acc)
+        elif self.halo:
+            self._run_halo(K, acc)
         for k in range(0 if (self.halo or self.overlap) else K):
             for i, p in enumerate(self.pencil):
                 p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
@@ -439,6 +442,9 @@ class ShardedAAR:
         import torch
         N = self.N
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
+        ns, W = self.geo.n_slab, self.geo.dims[-1]
+        first = [rk > 0 for rk in self.ranks]
+        has_halo = [bool(self.geo.halo(rk)) for rk in self.ranks]
         S, C = self._stream_pair()
         cuda = S is not None
 
@@ -469,16 +475,28 @@ class ShardedAAR:
                     for i, s in enumerate(self.slab):
                         s.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
                         acc[i][k] += self._bufs[i]["Ns"][0]
+                    if self.halo:  # straddling paths' d on the halo row -> the owner's first row
+                        self.comm.send_next(
+                            [b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)],
+                            [hr if f else None for hr, f in zip(self._hrow, first)])
+                        for i, b in enumerate(self._bufs):
+                            if first[i]:
+                                b["Gs"][:W] += self._hrow[i]
                     if cuda:
                         S.wait_event(ev_a)
+                    for i, b in enumerate(self._bufs):
+                        b["Gs"][:ns].view(dz, P, cp).add_(self._recv_s[i].transpose(0, 1))
+                        self._send_g[i].copy_(b["Gs"][:ns].view(dz, P, cp).transpose(0, 1))
+                    if self.halo:  # the owner's complete first-row g -> the halo row
+                        self.comm.send_prev(
+                            [b["Gs"][:W] if f else None for b, f in zip(self._bufs, first)],
+                            [b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)])
                     for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
-                        b["Gs"].view(dz, P, cp).add_(self._recv_s[i].transpose(0, 1))
                         if hasattr(s, "host_buffer"):
                             s.apply_g_host(b["Gs"].numpy())
                         else:
                             s.apply_g(b["Gs"].data_ptr())
                         acc[i][k] += b["Ns"][1]
-                        self._send_g[i].copy_(b["Gs"].view(dz, P, cp).transpose(0, 1))
                     ev_j = torch.cuda.Event() if cuda else None
                     if cuda:
                         ev_j.record(S)

@@ -45,7 +45,7 @@ def _worker(rank, world, port, conn, dims, iters, q, overlap=False):
 
 @pytest.mark.parametrize("conn,dims,overlap", [("3D-6", (6, 8, 5), False), ("2D-4", (12, 10), False),
                                                ("2D-8", (12, 10), False), ("3D-6", (6, 8, 5), True),
-                                               ("2D-4", (12, 10), True)])
+                                               ("2D-4", (12, 10), True), ("2D-8", (12, 10), True)])
 def test_gloo_world2_matches_unsharded(conn, dims, overlap):
     import multiprocessing as mp
     from emu import EmuSolver
@@ -153,8 +153,6 @@ def test_virtual_ranks_on_one_gpu_match_single(P, conn, dims, overlap):
     from paracut_b200 import _native
     g = make_instance(SPEC[conn], seed=4, dims=dims)
     k = 25
-    if conn == "2D-8" and not overlap:
-        pytest.skip("2D-8 always runs the serial halo schedule")
     sh = ShardedAAR(g, LocalComm(P), range(P),
                     lambda sub: _native.GridSolver(sub, precision="f32"), device="cuda",
                     overlap=overlap)
