@@ -244,9 +244,7 @@ def run_sharded(args, world, rank, local):
     clocks.mark_start()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    stream = torch.cuda.current_stream()
-    if mode == "cuda-graph":
-        stream = sh._gstream
+    stream = torch.cuda.current_stream()  # CUDAGraph.replay launches on the current stream
     ev0.record(stream)
     if mode == "cuda-graph":
         sh.run_graph(args.steps)
