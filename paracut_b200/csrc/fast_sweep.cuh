@@ -49,9 +49,9 @@ constexpr int TP = 8;          // positions per tile
 constexpr int NT = 4;          // tiles in the ring
 constexpr int RL = TP * NT;    // ring length (positions)
 #ifndef PCB_SWEEP_WARPS
-#define PCB_SWEEP_WARPS 4
+#define PCB_SWEEP_WARPS 2
 #endif
-constexpr int WARPS = PCB_SWEEP_WARPS;  // warps per block (4 x 16 KB rings, 3 blocks/SM; 7 measured slower)
+constexpr int WARPS = PCB_SWEEP_WARPS;  // warps per block (2 x 16.5 KB rings, 6 blocks/SM; 1: 13 warps/SM, slower; 4: -1-2 %)
 constexpr int MWARPS = 4;               // warps per block of the merge kernel
 #ifndef PCB_SCAN_KEEP
 #define PCB_SCAN_KEEP 16  // a round ends when at most this many lanes still have data
@@ -140,6 +140,9 @@ __device__ __forceinline__ void cp8(void* dst, const void* src, bool pred) {
       " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(s),
       "l"(src), "r"((int)pred));
 }
+__device__ __forceinline__ void l2_prefetch(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_wait(int pending) {
   switch (pending) {
@@ -198,6 +201,14 @@ __device__ __noinline__ double z_global(const Args& A, int64_t fi, int64_t nd) {
 }
 __device__ __noinline__ double a_global(const Args& A, int64_t fi) { return (double)A.wf[fi]; }
 
+// monitor terms with explicit FMAs (the TU is built with -fmad=false for the
+// exact path; the fp32-state monitor has no bitwise contract)
+__device__ __forceinline__ double nrm_d(double d, double acc) { return __fma_rn(d, d, acc); }
+// LAST role: 2 dcv g + r dcv^2 = dcv (2 g + r dcv)
+__device__ __forceinline__ double nrm_last(double dcv, double g, double rd, double acc) {
+  return __fma_rn(dcv, __fma_rn(rd, dcv, g + g), acc);
+}
+
 template <int ROLE>
 __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t nd, double fill) {
   const float pold = A.p[fi];
@@ -209,7 +220,7 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
   }
   const float p32 = (float)pn;
   const double d = (double)p32 - (double)pold;
-  double nrm = d * d;
+  double nrm = nrm_d(d, 0.0);
   A.p[fi] = p32;
   if (ROLE == FIRST) {
     A.G[nd] = (float)d;
@@ -223,7 +234,7 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
     const double dcv = (xn - g) * A.inv_r;
     A.c[nd] = cz + dcv;
     if (A.export_g) A.G[nd] = g32;
-    nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
+    nrm = nrm_last(dcv, g, A.rd, nrm);
   }
   return nrm;
 }
@@ -266,6 +277,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   auto node = [&](int b, int pos) { return b + pos * ns32 + zz32 * ((pos + ph32) & 1); };
   // mode B (row-like families): lane works on chains 8*(lane/8) + ib, ib < 8;
   // their node bases are fixed for the whole launch
+  const int b0 = __shfl_sync(0xffffffffu, base32, 0);  // lane 0's chain base
   int bB[8];
   if (ROWLIKE) {
 #pragma unroll
@@ -354,6 +366,19 @@ __global__ void __launch_bounds__(WARPS * 32)
   auto issue = [&](int T) {
     const int k0 = T * TP;
     PCB_CNT(3, 1);
+    if (ROLE == MID || ROLE == LAST) {
+      // pull the tile's retire-only inputs (G, X: natural layout) towards L2
+      // now, so the register prefetch a round before retirement hits L2
+      if (!ROWLIKE) {  // 32 chains = 32 consecutive nodes per position: lanes 0-7 G, 8-15 X
+        const int q = lane & 7, pos = k0 + q;
+        if (warp_live && pos < m && (lane < 8 || (ROLE == LAST && lane < 16)))
+          l2_prefetch((lane < 8 ? (const void*)(A.G + node(b0, pos))
+                                : (const void*)(A.X + node(b0, pos))));
+      } else if (valid && k0 < m) {  // each lane: its chain's 8 positions
+        l2_prefetch(A.G + node(base32, k0));
+        if (ROLE == LAST) l2_prefetch(A.X + node(base32, k0));
+      }
+    }
     if (use_tma) {  // one elected lane moves the three (8 x 32) boxes of the tile
       if (lane == 0) {
         const unsigned bar = (unsigned)__cvta_generic_to_shared(&mbar[(T - t_first) & (NT - 1)]);
@@ -438,10 +463,15 @@ __global__ void __launch_bounds__(WARPS * 32)
     PCB_CNT(4, 1);
     if (pre_tile != T) prefetch(T);
     const int k0 = T * TP;
+    // positions of this tile my chain emitted: [max(start, k0), min(stop, i0))
+    const int elo = max(start, k0) - k0, ehi = min(min(stop, i0), k0 + TP) - k0;
+    const unsigned emask = (has && ehi > elo) ? (((1u << ehi) - 1u) & ~((1u << elo) - 1u)) : 0u;
+    double na = 0.0, nb = 0.0;  // two monitor accumulators: shorter dependency chains
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
-      if (has && pos >= start && pos < stop && pos < i0) {
+      double& nq = (q & 1) ? nb : na;
+      if ((emask >> q) & 1u) {
         const int slot = pos & (RL - 1);
         const int ix = rx(lane, pos);
         const double zj = rz[ix];
@@ -457,7 +487,7 @@ __global__ void __launch_bounds__(WARPS * 32)
           const float pold = rp[ix];
           const float p32 = (float)pn;
           const double d = (double)p32 - (double)pold;
-          nrm += d * d;
+          nq = nrm_d(d, nq);
           A.p[(pos * C32 + c32)] = p32;
           if (!ROWLIKE) {
             const int nd = node(base32, pos);
@@ -473,7 +503,7 @@ __global__ void __launch_bounds__(WARPS * 32)
               const double dcv = (xn - g) * A.inv_r;
               A.c[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
               if (A.export_g) A.G[nd] = g32;
-              nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
+              nq = nrm_last(dcv, g, A.rd, nq);
             }
           } else {
             ra[ix] = (float)d;
@@ -483,9 +513,6 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     smask &= ~(0xffu << ((k0 & (RL - 1))));
     if (ROWLIKE) {
-      // positions of this tile my chain emitted: [max(start, k0), min(stop, i0))
-      const int lo = max(start, k0) - k0, hi = min(min(stop, i0), k0 + TP) - k0;
-      const unsigned emask = (has && hi > lo) ? (((1u << hi) - 1u) & ~((1u << lo) - 1u)) : 0u;
       __syncwarp();
       const int q = lane & 7;
       const int pos = k0 + q;
@@ -511,12 +538,14 @@ __global__ void __launch_bounds__(WARPS * 32)
             const double dcv = (xn - g) * A.inv_r;
             A.c[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
             if (A.export_g) A.G[nd] = g32;
-            nrm += 2.0 * dcv * g + A.rd * dcv * dcv;
+            double& nq = (ib & 1) ? nb : na;
+            nq = nrm_last(dcv, g, A.rd, nq);
           }
         }
       }
       __syncwarp();
     }
+    nrm += na + nb;
   };
 
   // one round of scanning; LAG: some lane's anchor is below the ring
