@@ -53,8 +53,11 @@ constexpr int RL = TP * NT;    // ring length (positions)
 #endif
 constexpr int WARPS = PCB_SWEEP_WARPS;  // warps per block (2 x 16.5 KB rings, 6 blocks/SM; 1: 13 warps/SM, slower; 4: -1-2 %)
 constexpr int MWARPS = 4;               // warps per block of the merge kernel
+#ifndef PCB_SCAN_UNROLL
+#define PCB_SCAN_UNROLL 2  // trips per exit vote (lag-free rounds)
+#endif
 #ifndef PCB_SCAN_KEEP
-#define PCB_SCAN_KEEP 16  // a round ends when at most this many lanes still have data
+#define PCB_SCAN_KEEP 20  // a round ends when at most this many lanes still have data (16-20 flat)
 #endif
 static_assert(RL == 32, "swizzle and start masks assume a 32-position ring");
 static_assert(TP == 8, "mode-B lane mapping assumes 8-position tiles");
@@ -563,12 +566,8 @@ __global__ void __launch_bounds__(WARPS * 32)
       t = zn;
       fresh = false;
     }
-    for (;;) {
+    auto trip = [&]() {
       const bool act = k < lim;
-      const int nact = __popc(__ballot_sync(0xffffffffu, act));
-      if (nact <= keep_min) break;
-      PCB_CNT(0, 1);
-      PCB_CNT(1, nact);
       if (act) {
         const int kp = k;
         double zabs = zn;
@@ -680,6 +679,18 @@ __global__ void __launch_bounds__(WARPS * 32)
           fresh = bend && !triv && k >= lim;
         }
       }
+    };
+    for (;;) {
+      const int nact = __popc(__ballot_sync(0xffffffffu, k < lim));
+      if (nact <= keep_min) break;
+      PCB_CNT(0, 1);
+      PCB_CNT(1, nact);
+      trip();
+      // more trips per exit vote (the vote, popcount and loop branch are ~5
+      // of the ~110 instructions of a trip); a round may run a few trips past
+      // the keep threshold
+#pragma unroll
+      for (int u = 1; u < (LAG ? 1 : PCB_SCAN_UNROLL); ++u) trip();
     }
   };
 
