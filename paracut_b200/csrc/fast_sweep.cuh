@@ -332,8 +332,12 @@ __global__ void __launch_bounds__(WARPS * 32)
   double t = 0.0;          // z at the anchor: scan values are z - t
   bool fresh = true;       // t is taken from the first gate after a (re)start
   R skr = R(0);            // running sum of (z - t) minus the anchor value
-  R cs = R(0), Lc = R(0);  // min slope to the ceiling points; cs * (k - i0)
-  R fs = R(0), Lf = R(0);  // max slope to the floor points;   fs * (k - i0)
+  // Cone state.  "No ceiling / floor point yet" (a fresh anchor) is Lc = +inf,
+  // Lf = fs = -inf: the next gate's cone tests then accept its tube points
+  // and no bend test can fire, without index sentinels in the trip.
+  constexpr R RINF = R(__builtin_huge_valf());
+  R cs = R(0), Lc = RINF;  // min slope to the ceiling points; cs * (k - i0)
+  R fs = -RINF, Lf = -RINF;  // max slope to the floor points; fs * (k - i0)
   unsigned smask = 0u;        // segment starts inside the ring (bit = slot)
   double zs = 0.0, qs = 0.0;  // retire carry: z at the current segment start, q there
 
@@ -596,21 +600,23 @@ __global__ void __launch_bounds__(WARPS * 32)
         const R sE = at_stop ? skr + eoff : skr;  // string value required at an end gate
         // ceiling: keep the minimum slope from the anchor
         const R u = sE + rk;
-        const bool cu = c0x < 0 || u <= Lc;
+        const bool cu = u <= Lc;
         c0x = cu ? k : c0x;
         cs = cu ? u * inv : cs;
         Lc = cu ? u : Lc;
-        const bool b1 = f0x >= 0 && cs < fs;  // ceiling dips under the floor cone
+        const bool b1 = cs < fs;  // ceiling dips under the floor cone
         // floor: keep the maximum slope (not pushed when b1 already bends)
         const R l = sE - rk;
-        const bool fu = !b1 && (f0x < 0 || l >= Lf);
+        const bool fu = !b1 && l >= Lf;
         f0x = fu ? k : f0x;
         fs = fu ? l * inv : fs;
         Lf = fu ? l : Lf;
         const bool b2 = !b1 && fs > cs;       // floor rises over the ceiling cone
         const bool e = !b1 && !b2 && zw;  // piece end: S_k is mandatory
-        const bool ec = e && c0x != k && Lc < sE;
-        const bool ef = e && !ec && f0x != k && Lf > sE;
+        // (a ceiling / floor point taken at this gate has Lc = sE + rk >= sE /
+        // Lf = sE - rk <= sE, so these tests need no "is it this gate" check)
+        const bool ec = e && Lc < sE;
+        const bool ef = e && !ec && Lf > sE;
         const bool bend = b1 || b2 || e;
 #ifdef PCB_COUNT
         if (bend) atomicAdd(&g_count[2], 1ull);
@@ -646,9 +652,10 @@ __global__ void __launch_bounds__(WARPS * 32)
         k = bend ? bk : k;
         if (LAG) fresh = bend;
         skr = bend ? nskr : skr;
-        // c0x / f0x = -1 make the next gate overwrite cs, Lc, fs, Lf
-        c0x = bend ? -1 : c0x;
-        f0x = bend ? -1 : f0x;
+        // a fresh anchor: the next gate overwrites cs, Lc, fs, Lf
+        Lc = bend ? RINF : Lc;
+        Lf = bend ? -RINF : Lf;
+        fs = bend ? -RINF : fs;
         const int ixn = rx(lane, k);
         zn = rz[ixn];
         an = ra[ixn];
