@@ -262,6 +262,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   // block); row-like families keep [lane][pos] with the XOR swizzle that
   // their 8-lanes-along-a-row loads need
   auto rx = [](int l, int pos) { return ROWLIKE ? rix(l, pos) : pix(l, pos); };
+  // ring index of position k0 + q of a tile (k0 a multiple of TP, q < TP): in
+  // the [pos][lane] layout the tile's rows are 32 apart with no wrap inside a
+  // tile, so the per-q offset folds into the shared-memory address immediate
+  auto tix = [&](int k0, int q) { return ROWLIKE ? rix(lane, k0 + q) : pix(lane, k0) + (q << 5); };
   const bool use_tma = !ROWLIKE && M.tma;
   unsigned long long* mbar =
       reinterpret_cast<unsigned long long*>(base + 32 * RL * (ROLE == SHADOW ? 24 : 16));
@@ -277,7 +281,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int C32 = (int)F.C, c32 = (int)c;
   const int ns32 = (int)F.ns, zz32 = (int)F.zz, ph32 = F.phase;
   const int base32 = valid ? (int)fam_base(F, c) : 0;
-  auto node = [&](int b, int pos) { return b + pos * ns32 + zz32 * ((pos + ph32) & 1); };
+  // zig-zag families are row-like, so strided families have no zig-zag term
+  auto node = [&](int b, int pos) {
+    return ROWLIKE ? b + pos * ns32 + zz32 * ((pos + ph32) & 1) : b + pos * ns32;
+  };
   // mode B (row-like families): lane works on chains 8*(lane/8) + ib, ib < 8;
   // their node bases are fixed for the whole launch
   const int b0 = __shfl_sync(0xffffffffu, base32, 0);  // lane 0's chain base
@@ -460,7 +467,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   auto to_z = [&](int T) {
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
-      const int ix = rx(lane, T * TP + q);
+      const int ix = tix(T * TP, q);
       rz[ix] = (double)rp[ix] + rz[ix];
     }
   };
@@ -474,15 +481,15 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int elo = max(start, k0) - k0, ehi = min(min(stop, i0), k0 + TP) - k0;
     const unsigned emask = (has && ehi > elo) ? (((1u << ehi) - 1u) & ~((1u << elo) - 1u)) : 0u;
     double na = 0.0, nb = 0.0;  // two monitor accumulators: shorter dependency chains
+    const unsigned stile = smask >> (k0 & (RL - 1));  // segment starts of this tile (bit q)
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
       double& nq = (q & 1) ? nb : na;
       if ((emask >> q) & 1u) {
-        const int slot = pos & (RL - 1);
-        const int ix = rx(lane, pos);
+        const int ix = tix(k0, q);
         const double zj = rz[ix];
-        if ((smask >> slot) & 1u) {
+        if ((stile >> q) & 1u) {
           zs = zj;
           qs = (ROLE == SHADOW) ? rf[ix] : (double)ra[ix];
         }
