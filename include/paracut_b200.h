@@ -175,6 +175,24 @@ int pcb_check(pcb_solver *h, int nthr, const double *thr, double *energy, double
 /* Copy the current check's labels for threshold t (uint8[n], or packed bits
  * MSB-first like np.packbits when packed=1) and x (fp64[n]) to host (each nullable). */
 int pcb_get_check(pcb_solver *h, int t, uint8_t *labels, int packed, double *x);
+/* Solve log (extension; replaces per-check host copies with one read at the
+ * end, as solvers.py:170-209 only needs them in finish()):
+ *   pcb_log_start     start logging (clears the log): pcb_aar_run / pcb_apply
+ *                     called with a NULL step_norms append their step norms
+ *                     to a device log instead of the handle's scratch slot
+ *   pcb_log_stop      stop logging (the log stays readable)
+ *   pcb_log_norms     copy min(cap, count) logged norms to out; *count = total
+ *   pcb_log_labels    append the current check's packed labels for threshold
+ *                     t (np.packbits order) to the device log; *slot = index
+ *   pcb_log_label_get copy one logged labeling (packed, (n+7)/8 bytes) to host
+ *   pcb_log_jaccard   out[i] = jaccard_distance(slot i, ref) for every slot
+ *                     (certify.py:68-78 on packed bits, exact integer counts) */
+int pcb_log_start(pcb_solver *h);
+int pcb_log_stop(pcb_solver *h);
+int pcb_log_norms(pcb_solver *h, double *out, int64_t cap, int64_t *count);
+int pcb_log_labels(pcb_solver *h, int t, int64_t *slot);
+int pcb_log_label_get(pcb_solver *h, int64_t slot, uint8_t *packed);
+int pcb_log_jaccard(pcb_solver *h, const uint8_t *ref_packed, double *out, int64_t cap);
 /* Keep the current check as the best iterate / fetch the kept one. */
 int pcb_keep_best(pcb_solver *h, int t);
 int pcb_get_best(pcb_solver *h, uint8_t *labels, double *x);

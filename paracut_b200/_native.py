@@ -76,6 +76,12 @@ def _declare(L):
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
     L.pcb_set_owned.argtypes = [P, I64]
+    L.pcb_log_start.argtypes = [P]
+    L.pcb_log_stop.argtypes = [P]
+    L.pcb_log_norms.argtypes = [P, P, I64, ctypes.POINTER(I64)]
+    L.pcb_log_labels.argtypes = [P, INT, ctypes.POINTER(I64)]
+    L.pcb_log_label_get.argtypes = [P, I64, P]
+    L.pcb_log_jaccard.argtypes = [P, P, P, I64]
     L.pcb_launch_count.argtypes = [P]
     L.pcb_launch_count.restype = I64
     L.pcb_reset_launch_count.argtypes = [P]
@@ -88,7 +94,9 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_aar_step", "pcb_set_family_mask", "pcb_apply_g", "pcb_device_buffer",
            "pcb_shadow", "pcb_shadow_get", "pcb_shadow_delta", "pcb_apply", "pcb_check", "pcb_get_check", "pcb_keep_best",
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
-           "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned")
+           "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
+           "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
+           "pcb_log_jaccard")
 
 
 def lib():
@@ -296,10 +304,49 @@ class GridSolver:
         check(lib().pcb_shadow_delta(self.handle, ptr(d)))
         return float(d[0])
 
-    def apply(self):
+    def apply(self, norm=True):
+        """One AAR update from the current shadow; its step norm (None when
+        norm=False: with the solve log on it is logged on the device)."""
+        if not norm:
+            check(lib().pcb_apply(self.handle, None))
+            return None
         out = np.empty(1)
         check(lib().pcb_apply(self.handle, ptr(out)))
         return float(out[0])
+
+    # ---- solve log (pcb_log_*): step norms and check labelings kept on the
+    # device until the solve ends
+    def log_start(self):
+        check(lib().pcb_log_start(self.handle))
+
+    def log_stop(self):
+        check(lib().pcb_log_stop(self.handle))
+
+    def log_norms(self):
+        cnt = I64(0)
+        check(lib().pcb_log_norms(self.handle, None, 0, ctypes.byref(cnt)))
+        out = np.empty(max(int(cnt.value), 1))
+        check(lib().pcb_log_norms(self.handle, ptr(out), int(cnt.value), ctypes.byref(cnt)))
+        return out[:int(cnt.value)]
+
+    def log_labels(self, t):
+        """Append the current check's packed labels (threshold t); returns the slot."""
+        slot = I64(0)
+        check(lib().pcb_log_labels(self.handle, int(t), ctypes.byref(slot)))
+        return int(slot.value)
+
+    def log_label_get(self, slot):
+        out = np.empty((self.n + 7) // 8, dtype=np.uint8)
+        check(lib().pcb_log_label_get(self.handle, int(slot), ptr(out)))
+        return out
+
+    def log_jaccard(self, ref_packed, count):
+        ref = np.ascontiguousarray(ref_packed, dtype=np.uint8)
+        if ref.size != (self.n + 7) // 8:
+            raise ValueError("packed reference has %d bytes, expected %d" % (ref.size, (self.n + 7) // 8))
+        out = np.empty(max(int(count), 1))
+        check(lib().pcb_log_jaccard(self.handle, ptr(ref), ptr(out), int(count)))
+        return out[:int(count)]
 
     def check(self, thresholds):
         thr = _f64(thresholds)

@@ -733,6 +733,36 @@ __global__ void k_labels(const uint8_t* bits, int64_t n, int t, uint8_t* lab) {
     lab[i] = (bits[i] >> t) & 1u;
 }
 
+// Jaccard distance of every logged packed labeling (slot i at lab + i * nb)
+// against ref: one block per slot, integer popcounts (exact).
+__global__ void k_log_jaccard(const uint8_t* lab, const uint8_t* ref, int64_t nb, double* out) {
+  const uint8_t* a = lab + (int64_t)blockIdx.x * nb;
+  unsigned long long inter = 0, uni = 0;
+  for (int64_t q = threadIdx.x; q < nb; q += blockDim.x) {
+    const unsigned x = a[q], y = ref[q];
+    inter += __popc(x & y);
+    uni += __popc(x | y);
+  }
+  __shared__ unsigned long long si[32], su[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    inter += __shfl_down_sync(0xffffffffu, inter, o);
+    uni += __shfl_down_sync(0xffffffffu, uni, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    si[threadIdx.x >> 5] = inter;
+    su[threadIdx.x >> 5] = uni;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ti = 0, tu = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      ti += si[w];
+      tu += su[w];
+    }
+    out[blockIdx.x] = tu == 0 ? 0.0 : 1.0 - (double)ti / (double)tu;
+  }
+}
+
 // np.packbits order: byte q holds labels 8q..8q+7, label 8q in bit 7.
 __global__ void k_pack(const uint8_t* bits, int64_t n, int t, uint8_t* out) {
   const int64_t nb = (n + 7) / 8;
@@ -871,6 +901,26 @@ struct DBuf {
 
 #include "hostio.cuh"
 
+// grow b to hold `need` elements, keeping its first `used` (stream-ordered copy)
+template <class T>
+int grow_keep(DBuf<T>& b, size_t need, size_t used, cudaStream_t st, size_t min_cap = 0) {
+  if (b.n >= need && b.p) return 0;
+  DBuf<T> nb;
+  size_t cap = b.n * 2;
+  if (cap < need) cap = need;
+  if (cap < min_cap) cap = min_cap;
+  if (int e = nb.alloc(cap)) return e;
+  if (used > 0 && b.p) {
+    cudaError_t ce = cudaMemcpyAsync(nb.p, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail(PCB_E_CUDA, "log growth: %s", cudaGetErrorString(ce));
+  }
+  std::swap(b.p, nb.p);
+  std::swap(b.n, nb.n);
+  std::swap(b.pooled, nb.pooled);
+  return 0;  // nb now owns (and frees) the old storage
+}
+
 }  // namespace
 
 struct pcb_solver {
@@ -921,6 +971,13 @@ struct pcb_solver {
   DBuf<int> sp_cx, sp_fx;
   DBuf<double> sp_cy, sp_fy;
   DBuf<uint8_t> packed;
+  // solve log (pcb_log_*): step norms and packed check labelings stay on the
+  // device until the solve ends, so check cycles need one host sync only
+  bool logging = false;
+  DBuf<double> normlog;
+  int64_t nlog = 0;
+  DBuf<uint8_t> lablog;
+  int64_t nlab = 0;
   int64_t spill_per = 0;  // spill entries per thread
   unsigned fmask = 0xfu;  // families swept by this handle (sharded runs split them)
   int nbk[MAXR]{};        // fp32 path: blocks per chain (intra-chain split), 1 = whole chains
@@ -1962,15 +2019,21 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   if (int e = set_dev(h)) return e;
   if ((int64_t)h->norms.n < iters)
     if (int e = h->norms.alloc(iters)) return e;
+  const bool to_log = h->logging && !step_norms;
+  if (to_log)
+    if (int e = grow_keep(h->normlog, (size_t)(h->nlog + iters), (size_t)h->nlog, h->stream, 4096))
+      return e;
+  double* nout = to_log ? h->normlog.p + h->nlog : h->norms.p;
   for (int64_t k = 0; k < iters; ++k) {
     int rc;
     if (h->precision == PCB_F64) {
       if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
-      if ((rc = update_exact(h, h->norms.p + k))) return rc;
+      if ((rc = update_exact(h, nout + k))) return rc;
     } else {
-      if ((rc = step_fast(h, h->norms.p + k, flags))) return rc;
+      if ((rc = step_fast(h, nout + k, flags))) return rc;
     }
   }
+  if (to_log) h->nlog += iters;
   h->have_shadow = false;
   h->y_valid = false;
   if (step_norms) {
@@ -2048,11 +2111,17 @@ int pcb_apply(pcb_solver* h, double* step_norm) {
   if (!h->have_shadow) return fail(PCB_E_STATE, "apply needs a current shadow (call pcb_shadow)");
   if (int e = set_dev(h)) return e;
   int rc;
+  const bool to_log = h->logging && !step_norm;
+  if (to_log)
+    if (int e = grow_keep(h->normlog, (size_t)(h->nlog + 1), (size_t)h->nlog, h->stream, 4096))
+      return e;
+  double* nout = to_log ? h->normlog.p + h->nlog : h->norms.p;
   if (h->precision == PCB_F64) {
-    if ((rc = update_exact(h, h->norms.p))) return rc;
+    if ((rc = update_exact(h, nout))) return rc;
   } else {
-    if ((rc = apply_fast(h, h->norms.p))) return rc;
+    if ((rc = apply_fast(h, nout))) return rc;
   }
+  if (to_log) h->nlog += 1;
   h->have_shadow = false;
   if (step_norm) {
     CUDA_TRY(hostio::d2h(step_norm, h->norms.p, sizeof(double), h->stream));
@@ -2123,6 +2192,80 @@ int pcb_get_check(pcb_solver* h, int t, uint8_t* labels, int packed, double* x) 
   }
   if (x)
     CUDA_TRY(hostio::d2h(x, h->xcur.p, h->n * sizeof(double), h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_log_start(pcb_solver* h) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  h->logging = true;
+  h->nlog = 0;
+  h->nlab = 0;
+  return 0;
+}
+
+int pcb_log_stop(pcb_solver* h) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  h->logging = false;
+  return 0;
+}
+
+int pcb_log_norms(pcb_solver* h, double* out, int64_t cap, int64_t* count) {
+  if (!h || !count) return fail(PCB_E_ARG, "null argument");
+  if (int e = set_dev(h)) return e;
+  *count = h->nlog;
+  const int64_t m = h->nlog < cap ? h->nlog : cap;
+  if (m > 0) {
+    if (!out) return fail(PCB_E_ARG, "null output");
+    CUDA_TRY(hostio::d2h(out, h->normlog.p, (size_t)m * sizeof(double), h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_log_labels(pcb_solver* h, int t, int64_t* slot) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (!h->have_check) return fail(PCB_E_STATE, "no current check");
+  if (t < 0 || t >= h->check_T) return fail(PCB_E_ARG, "threshold index out of range");
+  if (int e = set_dev(h)) return e;
+  const int64_t nb = (h->n + 7) / 8;
+  if (int e = grow_keep(h->lablog, (size_t)((h->nlab + 1) * nb), (size_t)(h->nlab * nb), h->stream,
+                        (size_t)(32 * nb)))
+    return e;
+  k_pack<<<grid_for(nb, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t,
+                                                              h->lablog.p + h->nlab * nb);
+  LAUNCH_CHECK(h);
+  if (slot) *slot = h->nlab;
+  h->nlab += 1;
+  return 0;
+}
+
+int pcb_log_label_get(pcb_solver* h, int64_t slot, uint8_t* packed) {
+  if (!h || !packed) return fail(PCB_E_ARG, "null argument");
+  if (slot < 0 || slot >= h->nlab) return fail(PCB_E_ARG, "label slot out of range");
+  if (int e = set_dev(h)) return e;
+  const int64_t nb = (h->n + 7) / 8;
+  CUDA_TRY(hostio::d2h(packed, h->lablog.p + slot * nb, (size_t)nb, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int pcb_log_jaccard(pcb_solver* h, const uint8_t* ref_packed, double* out, int64_t cap) {
+  if (!h || !ref_packed) return fail(PCB_E_ARG, "null argument");
+  if (cap < h->nlab) return fail(PCB_E_ARG, "output holds %lld of %lld slots", (long long)cap,
+                                 (long long)h->nlab);
+  if (h->nlab == 0) return 0;
+  if (!out) return fail(PCB_E_ARG, "null output");
+  if (int e = set_dev(h)) return e;
+  const int64_t nb = (h->n + 7) / 8;
+  if ((int64_t)h->packed.n < nb)
+    if (int e = h->packed.alloc(nb)) return e;
+  if ((int64_t)h->parts.n < h->nlab)
+    if (int e = h->parts.alloc(h->nlab)) return e;
+  CUDA_TRY(hostio::h2d(h->packed.p, ref_packed, (size_t)nb, h->stream));
+  k_log_jaccard<<<(unsigned)h->nlab, 256, 0, h->stream>>>(h->lablog.p, h->packed.p, nb, h->parts.p);
+  LAUNCH_CHECK(h);
+  CUDA_TRY(hostio::d2h(out, h->parts.p, (size_t)h->nlab * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }

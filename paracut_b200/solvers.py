@@ -203,7 +203,27 @@ class _Driver:
         self.kmax = cfg.max_iters
         self.stall = 0  # > 0: leave the loop once the best gap stalls for this many checks
         self._best_hist = []
+        self.log = False  # solve log on the device (start_log)
         self.t0 = time.perf_counter()
+
+    def start_log(self):
+        """Keep step norms and check labelings on the device (pcb_log_*): a check
+        cycle then syncs the host once, for the certificate it must act on."""
+        self.log = True
+        self.solver.log_start()
+
+    def flush_norms(self):
+        """Move the current handle's logged step norms into the monitor."""
+        if self.log:
+            self.record("aar_step_norm", self.solver.log_norms())
+            self.solver.log_stop()
+
+    def switch_solver(self, S):
+        """Continue on another handle (fp64 polish), keeping the log going."""
+        self.flush_norms()
+        self.solver = S
+        if self.log:
+            S.log_start()
 
     def warm_or_cold(self):
         ws = self.cfg.warm_start
@@ -242,6 +262,9 @@ class _Driver:
         if self.cfg.reference is not None:
             lab = self.solver.check_labels(t)
             jac = jaccard_distance(lab, self.cfg.reference)
+        elif self.log:
+            packed = (self.solver, self.solver.log_labels(t))
+            self._labs.append(packed)
         else:
             packed = self.solver.check_labels(t, packed=True)
             self._labs.append(packed)
@@ -292,9 +315,23 @@ class _Driver:
         wall = time.perf_counter() - self.t0
         lab, x = (self.best_solver or self.solver).get_best()
         certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
-        if self.cfg.reference is None:
+        if self.cfg.reference is None and self.log:
+            self.flush_norms()
+            # jaccard against the best labeling, every logged slot of every
+            # handle in one device pass each
+            ref = self.best_packed[0].log_label_get(self.best_packed[1]) if self._labs else None
+            jac = {}
+            for h, _ in self._labs:
+                if id(h) not in jac:
+                    cnt = sum(1 for h2, _ in self._labs if h2 is h)
+                    jac[id(h)] = h.log_jaccard(ref, cnt)
+            for row, (h, slot) in zip(self.trace, self._labs):
+                row.jaccard = float(jac[id(h)][slot])
+        elif self.cfg.reference is None:
             for row, packed in zip(self.trace, self._labs):
                 row.jaccard = jaccard_packed(packed, self.best_packed)
+        elif self.log:
+            self.flush_norms()
         if state is None:
             state = _DeviceDualState(self.solver, self.g)
         return SolveResult(labeling=lab, tv_solution=x, energy=self.best_energy,
@@ -335,6 +372,7 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
     polish = cfg.precision == "f32" and cfg.polish_iters > 0
     if polish:
         drv.stall = cfg.polish_stall
+    drv.start_log()
     k = _loop(drv, S, k)
     drv.stall = 0
     if polish and not drv.stopped:
@@ -343,7 +381,7 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
         S64 = (_make64() if _make64 is not None else
                _native.GridSolver(g, precision="f64", device=cfg.device))
         S64.set_z(S.get_z())
-        drv.solver = S64
+        drv.switch_solver(S64)
         drv.kmax = k + cfg.polish_iters
         drv.record("polish_start", k)
         _loop(drv, S64, k)
@@ -357,11 +395,17 @@ def _loop(drv, S, k):
             S.shadow()
             if drv.check(k) or k >= drv.kmax or drv.stalled():
                 return k
-            drv.record("aar_step_norm", S.apply())
+            if drv.log:
+                S.apply(norm=False)
+            else:
+                drv.record("aar_step_norm", S.apply())
             k += 1
         else:
             nxt = drv.next_due(k)
-            drv.record("aar_step_norm", S.run(nxt - k))
+            if drv.log:
+                S.run(nxt - k, norms=False)
+            else:
+                drv.record("aar_step_norm", S.run(nxt - k))
             k = nxt
 
 
