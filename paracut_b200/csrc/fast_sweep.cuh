@@ -336,8 +336,8 @@ __global__ void __launch_bounds__(WARPS * 32)
   // have start = stop = 0); it is never active again, and its whole range
   // counts as emitted
   int i0 = start, k = start, c0x = -1, f0x = -1;
+  int ixi0 = rx(lane, start);  // ring index of the anchor i0
   double t = 0.0;          // z at the anchor: scan values are z - t
-  bool fresh = true;       // t is taken from the first gate after a (re)start
   R skr = R(0);            // running sum of (z - t) minus the anchor value
   // Cone state.  "No ceiling / floor point yet" (a fresh anchor) is Lc = +inf,
   // Lf = fs = -inf: the next gate's cone tests then accept its tube points
@@ -573,10 +573,9 @@ __global__ void __launch_bounds__(WARPS * 32)
     double zn = rz[rx(lane, k)];
     float an = ra[rx(lane, k)];
     const int lim = min(avail_hi, stop);  // gates are consumed while k < lim
-    if (!LAG && fresh && k < lim) {  // first gate of the unit or after a lagging round
-      t = zn;
-      fresh = false;
-    }
+    // an anchor gate not consumed yet (unit start, or a restart whose gate
+    // was not loaded when the string bent): t is its z
+    if (!LAG && k == i0 && k < lim) t = zn;
     auto trip = [&]() {
       const bool act = k < lim;
       if (act) {
@@ -589,13 +588,10 @@ __global__ void __launch_bounds__(WARPS * 32)
           af = kp < m - 1 ? (float)a_global(A, fi) : 0.f;
         }
         k = kp + 1;
-        if (LAG) {
-          t = fresh ? zabs : t;
-          fresh = false;
-        }
+        if (LAG) t = kp == i0 ? zabs : t;  // the anchor gate itself
         skr += (R)(zabs - t);
         const bool at_stop = k == stop;  // forced end point (merge point or chain end)
-        const bool inner = k < stop;     // (stop <= m)
+        const bool inner = !at_stop;     // (k <= stop)
         const R rk = inner ? (R)af : R(0);
         // a zero weight (or the unit end) makes this gate a mandatory piece end;
         // after an earlier bend the rescan reaches the same gate again, so no
@@ -645,8 +641,9 @@ __global__ void __launch_bounds__(WARPS * 32)
           s0 = e2;
           if (s0 < bk) qv = (R)((rz[rx(lane, s0)] - t) - (double)fill);
         }
-        const bool mark = bend && s0 < stop && (!LAG || s0 < bk);
-        const int ixs = rx(lane, s0);
+        // (lag-free: s0 = i0 < k <= stop)
+        const bool mark = LAG ? (bend && s0 < stop && s0 < bk) : bend;
+        const int ixs = LAG ? rx(lane, s0) : ixi0;
         if (mark) {
           if (ROLE == SHADOW) rf[ixs] = (double)qv;
           else ra[ixs] = (float)qv;
@@ -657,13 +654,13 @@ __global__ void __launch_bounds__(WARPS * 32)
         const R nskr = tf ? ab : (tc ? -ab : R(0));
         i0 = bend ? bk : i0;
         k = bend ? bk : k;
-        if (LAG) fresh = bend;
         skr = bend ? nskr : skr;
         // a fresh anchor: the next gate overwrites cs, Lc, fs, Lf
         Lc = bend ? RINF : Lc;
         Lf = bend ? -RINF : Lf;
         fs = bend ? -RINF : fs;
         const int ixn = rx(lane, k);
+        ixi0 = bend ? ixn : ixi0;  // i0 = k = bk after a bend
         zn = rz[ixn];
         an = ra[ixn];
         // non-lagging: the anchor value of a restarted string is the next gate's
@@ -690,7 +687,6 @@ __global__ void __launch_bounds__(WARPS * 32)
             zn = rz[ix1];
             an = ra[ix1];
           }
-          fresh = bend && !triv && k >= lim;
         }
       }
     };
