@@ -674,7 +674,11 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
   const int nd = D.nd;
   const int64_t L = nd == 3 ? D.d[2] : D.d[1];
   const int64_t rows = nd == 3 ? D.d[0] * D.d[1] : D.d[0];
-  for (int64_t Rr = blockIdx.x; Rr < rows; Rr += gridDim.x) {
+  // one warp per grid row (the rows of a block in flight together: the
+  // label loads of a row are few and latency bound); lanes along the row
+  const int lane = threadIdx.x & 31, nwb = blockDim.x >> 5;
+  for (int64_t Rr = (int64_t)blockIdx.x * nwb + (threadIdx.x >> 5); Rr < rows;
+       Rr += (int64_t)gridDim.x * nwb) {
     int64_t co[2] = {Rr, 0};
     if (nd == 3) {
       co[0] = Rr / D.d[1];
@@ -707,7 +711,8 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
       const int64_t lenL = L - (oL < 0 ? -oL : oL), loL = oL >= 0 ? 0 : -oL;
       const double* av = dw.p[k] + erow * lenL - loL;  // element (erow, x - loL)
       const uint8_t* bn = bits + base + joff;
-      for (int64_t x = loL + threadIdx.x; x < loL + lenL; x += blockDim.x) {
+#pragma unroll 4
+      for (int64_t x = loL + lane; x < loL + lenL; x += 32) {
         const unsigned diff = (unsigned)bits[base + x] ^ (unsigned)bn[x];
         if (diff) {
           const double a = av[x];
