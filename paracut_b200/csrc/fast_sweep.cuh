@@ -193,9 +193,10 @@ __device__ __forceinline__ int pix(int l, int pos) {
 
 template <int ROLE>
 __host__ __device__ constexpr int ring_bytes_host() {
-  // rz f64, rp f32, ra f32 (+ rf f64 for SHADOW), + NT tile mbarriers, padded
+  // rz f64, rp f32, ra f32 (SHADOW keeps its fp64 segment values split over
+  // the dead rp / ra slots), + NT tile mbarriers, padded
   // to 128 B so every warp's tile slots stay TMA-aligned
-  return 32 * RL * (8 + 4 + 4 + (ROLE == SHADOW ? 8 : 0)) + 128;
+  return 32 * RL * (8 + 4 + 4) + 128;
 }
 
 // lagging-lane accessors (positions below the ring), kept out of line
@@ -254,8 +255,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 
   unsigned char* base = smem_raw + (size_t)wib * ring_bytes_host<ROLE>();
   double* rz = reinterpret_cast<double*>(base);
-  double* rf = rz + 32 * RL;  // SHADOW only
-  float* rp = reinterpret_cast<float*>(base + 32 * RL * (ROLE == SHADOW ? 16 : 8));
+  float* rp = reinterpret_cast<float*>(base + 32 * RL * 8);
   float* ra = rp + 32 * RL;
   // ring layout: [pos][lane] rows of 32 for strided families (every access is
   // lane-contiguous, and a (positions x 32 chains) box is one contiguous
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   auto tix = [&](int k0, int q) { return ROWLIKE ? rix(lane, k0 + q) : pix(lane, k0) + (q << 5); };
   const bool use_tma = !ROWLIKE && M.tma;
   unsigned long long* mbar =
-      reinterpret_cast<unsigned long long*>(base + 32 * RL * (ROLE == SHADOW ? 24 : 16));
+      reinterpret_cast<unsigned long long*>(base + 32 * RL * 16);
 
   const bool warp_live = c0 < F.C;
   const int nvalid = warp_live ? (int)min((int64_t)32, F.C - c0) : 0;
@@ -491,7 +491,9 @@ __global__ void __launch_bounds__(WARPS * 32)
         const double zj = rz[ix];
         if ((stile >> q) & 1u) {
           zs = zj;
-          qs = (ROLE == SHADOW) ? rf[ix] : (double)ra[ix];
+          // (SHADOW: the fp64 q split over the dead p / weight slots)
+          qs = (ROLE == SHADOW) ? __hiloint2double(__float_as_int(ra[ix]), __float_as_int(rp[ix]))
+                                : (double)ra[ix];
         }
         const double pn = (zj - zs) + qs;
         if (ROLE == SHADOW) {
@@ -645,7 +647,11 @@ __global__ void __launch_bounds__(WARPS * 32)
         const bool mark = LAG ? (bend && s0 < stop && s0 < bk) : bend;
         const int ixs = LAG ? rx(lane, s0) : ixi0;
         if (mark) {
-          if (ROLE == SHADOW) rf[ixs] = (double)qv;
+          if (ROLE == SHADOW) {  // fp64 q: low word in the p slot, high word in the weight slot
+            const double qd = (double)qv;
+            rp[ixs] = __int_as_float(__double2loint(qd));
+            ra[ixs] = __int_as_float(__double2hiint(qd));
+          }
           else ra[ixs] = (float)qv;
         }
         smask |= (unsigned)mark << (s0 & (RL - 1));

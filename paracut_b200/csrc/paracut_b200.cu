@@ -243,13 +243,16 @@ __global__ void k_reduce_norm(const double* parts, int64_t count, double* out, i
   const int64_t per = (count + blockDim.x - 1) / blockDim.x;
   const int64_t lo = threadIdx.x * per, hi = min(count, lo + per);
   for (int64_t k = lo; k < hi; ++k) acc += parts[k];
-  __shared__ double all[1024];
-  all[threadIdx.x] = acc;
+  // slices combined by a fixed shuffle tree (deterministic; a serial sum of
+  // 1024 values by one thread cost ~4 us per iteration)
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < (int)blockDim.x; ++k) t += all[k];
-    *out = do_sqrt ? sqrt(t) : t;
+  if (threadIdx.x < 32) {
+    double t = threadIdx.x < (blockDim.x >> 5) ? ws[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) *out = do_sqrt ? sqrt(t) : t;
   }
 }
 
@@ -257,8 +260,18 @@ __global__ void k_reduce_norm(const double* parts, int64_t count, double* out, i
 __global__ void k_reduce_cols(const double* parts, int nblocks, int nv, double* vals) {
   const int j = threadIdx.x;
   if (j >= nv) return;
+  // the same left-to-right sum, with the partials of 16 blocks loaded ahead
+  // of their additions (the loop was load-latency bound)
   double t = 0.0;
-  for (int b = 0; b < nblocks; ++b) t += parts[(int64_t)b * nv + j];
+  int b = 0;
+  for (; b + 16 <= nblocks; b += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = parts[(int64_t)(b + u) * nv + j];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) t += v[u];
+  }
+  for (; b < nblocks; ++b) t += parts[(int64_t)b * nv + j];
   vals[j] = t;
 }
 
@@ -486,7 +499,7 @@ constexpr int APPLY_TILE = 32;
 constexpr int APPLY_THREADS = 256;  // launch with exactly this many threads
 
 template <int R>
-__global__ void __launch_bounds__(APPLY_THREADS) k_apply_fast(
+__global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
     const double* __restrict__ y, float* __restrict__ p, double* __restrict__ cdrift,
     float* __restrict__ X, const double* __restrict__ w, int64_t n,
     const __grid_constant__ FamSet FS, const __grid_constant__ Dims D, double* parts) {
@@ -527,31 +540,32 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fast(
     // all loads of the warp's T/NW rows first (memory-level parallelism),
     // then the arithmetic and the stores
     // rows per batch: bounded so the register file holds two blocks per SM
-    constexpr int S = R >= 4 ? 2 : T / NW;
+    // (32-bit node / state indices: pcb_create keeps r * n below 2^31)
+    constexpr int S = 2;
 #pragma unroll 1
     for (int b0 = 0; b0 < T / NW; b0 += S) {
     double yv[S][R], wv[S], cv[S];
     float po[S][R];
-    int64_t qv[S][R];
+    int qv[S][R];
     bool in[S][R];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int64_t Rr = R0 + wp + (b0 + s) * NW, x = X0 + lane;
+      const int Rr = (int)R0 + wp + (b0 + s) * NW, x = (int)X0 + lane;
       const bool ok = Rr < rows && x < L;
-      const int64_t i = ok ? Rr * L + x : 0;
+      const int i = ok ? Rr * (int)L + x : 0;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const Fam& F = FS.f[j];
         yv[s][j] = ok ? y[j * n + i] : 0.0;
         if (fam_rowlike(F.kind)) {
-          const int64_t c = (F.kind == K_ZZ0 || F.kind == K_ZZ1) ? Rr - ((x + F.phase) & 1) : Rr;
+          const int c = (F.kind == K_ZZ0 || F.kind == K_ZZ1) ? Rr - ((x + F.phase) & 1) : Rr;
           in[s][j] = ok && c >= 0 && c < F.C;  // zig-zag border node: not in this family
-          qv[s][j] = c - (R0 - 1);              // tile row
+          qv[s][j] = c - ((int)R0 - 1);         // tile row
           po[s][j] = in[s][j] ? tile[j][qv[s][j]][lane] : 0.f;
         } else {
           // COL2 / Z3: family layout == node order; Y3: [y][z][x]
           in[s][j] = ok;
-          qv[s][j] = j * n + (F.kind == K_Y3 ? (Rr % D1) * D0L + (Rr / D1) * L + x : i);
+          qv[s][j] = j * (int)n + (F.kind == K_Y3 ? (Rr % (int)D1) * (int)D0L + (Rr / (int)D1) * (int)L + x : i);
           po[s][j] = ok ? p[qv[s][j]] : 0.f;
         }
       }
@@ -560,9 +574,9 @@ __global__ void __launch_bounds__(APPLY_THREADS) k_apply_fast(
     }
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      const int64_t Rr = R0 + wp + (b0 + s) * NW, x = X0 + lane;
+      const int Rr = (int)R0 + wp + (b0 + s) * NW, x = (int)X0 + lane;
       if (Rr >= rows || x >= L) continue;
-      const int64_t i = Rr * L + x;
+      const int i = Rr * (int)L + x;
       double g = 0.0, sp = 0.0;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
