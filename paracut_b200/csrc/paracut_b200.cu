@@ -631,6 +631,7 @@ __global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n
     th[t] = t < T ? thr[t] : 0.0;
   }
   double dual = 0.0, ww = 0.0, dd = 0.0;
+#pragma unroll 4
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     double s = y[i];
