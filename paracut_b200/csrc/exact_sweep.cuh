@@ -35,6 +35,9 @@ using fast::cp_wait;
 // than SMs; 2D grids have only ~side chains per family) are bound by one
 // warp's own latency and want the deeper 32-position ring.  All families of
 // a sweep are independent (y_j depends on z_j only) and run in one launch.
+#ifndef PCB_EXACT_UNROLL
+#define PCB_EXACT_UNROLL 1
+#endif
 #ifndef PCB_EXACT_KEEP
 #define PCB_EXACT_KEEP 16  // a round ends when at most this many lanes still have data
 #endif
@@ -213,10 +216,9 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
       zn = s_at(k, lo_pos);
       an = k < m - 1 ? a_at(k, lo_pos) : 0.0;
     }
-    for (;;) {
+    auto trip = [&]() {
       const bool act = !done && k < avail_hi;
-      if (__popc(__ballot_sync(0xffffffffu, act)) <= keep_min) break;
-      if (!act) continue;
+      if (!act) return;
       // ---- one gate of the reference loop (_kernels.py:41-95)
       ++k;
       const double v = zn;
@@ -412,6 +414,12 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
           }
         }
       }
+    };
+    for (;;) {
+      if (__popc(__ballot_sync(0xffffffffu, !done && k < avail_hi)) <= keep_min) break;
+      // PCB_EXACT_UNROLL trips per exit vote (same gates, fewer votes)
+#pragma unroll
+      for (int u = 0; u < PCB_EXACT_UNROLL; ++u) trip();
     }
   };
 
