@@ -495,6 +495,95 @@ __global__ void k_get_fast(const float* p, const double* cdrift, double* z, int6
 // coordinates x 32 last-axis positions) and those families' p go through a
 // shared-memory tile: both the family-layout and the node-order accesses are
 // coalesced.  Per-node arithmetic is the same as a plain node loop.
+// Check-iteration update for grids with one row-like family (2D-4 rows, 3D x;
+// family 0), in two coalesced passes instead of one tiled pass:
+//   k_apply_rows   32 x 32 (chain, position) tiles of family 0: its old state
+//                  goes to G in node order (fp32, exact), its new state
+//                  (float)y_0 to the family layout, both through shared memory;
+//   k_apply_nodes  node order: every other family's state is node-ordered up
+//                  to the 3D y permutation, so each node's update reads and
+//                  writes coalesced arrays only.
+// Same per-node arithmetic and family order as k_apply_fast.
+__global__ void __launch_bounds__(256) k_apply_rows(const double* __restrict__ y0,
+                                                    float* __restrict__ p0, float* __restrict__ G,
+                                                    int C, int L) {
+  __shared__ float tp[32][33];   // [pos][chain]: old state
+  __shared__ double ty[32][33];  // [chain][pos]: shadow
+  const int tiles_c = (C + 31) / 32;
+  const int tiles = tiles_c * ((L + 31) / 32);
+  const int tx = threadIdx.x & 31, ty8 = threadIdx.x >> 5;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int c0 = (t % tiles_c) * 32, x0 = (t / tiles_c) * 32;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = ty8 + 8 * k;  // pos row for p, chain row for y
+      const int pos = x0 + r, c = c0 + tx;
+      tp[r][tx] = (pos < L && c < C) ? p0[pos * C + c] : 0.f;
+      const int cc = c0 + r, xx = x0 + tx;
+      ty[r][tx] = (cc < C && xx < L) ? y0[cc * L + xx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = ty8 + 8 * k;
+      const int cc = c0 + r, xx = x0 + tx;  // node (chain cc, pos xx)
+      if (cc < C && xx < L) G[cc * L + xx] = tp[tx][r];
+      const int pos = x0 + r, c = c0 + tx;  // family slot (pos, chain c)
+      if (pos < L && c < C) p0[pos * C + c] = (float)ty[tx][r];
+    }
+    __syncthreads();
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256) k_apply_nodes(
+    const double* __restrict__ y, float* __restrict__ p, const float* __restrict__ G,
+    double* __restrict__ cdrift, float* __restrict__ X, const double* __restrict__ w, int n,
+    int L, int D1, int C1, double* parts) {
+  // rows of L nodes; 3D: row = z * D1 + y, family 1 (y lines) at [y][z][x]
+  const int rows = n / L;
+  float* p1 = p + (int64_t)n;       // family 1 state
+  float* p2 = p + 2 * (int64_t)n;   // family 2 state (3D z lines: node order)
+  const int lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nwg = gridDim.x * (blockDim.x >> 5);
+  double acc = 0.0;
+  for (int Rr = wg; Rr < rows; Rr += nwg) {
+    const int q1 = R == 3 ? (Rr % D1) * C1 + (Rr / D1) * L : Rr * L;  // family 1 row base
+#pragma unroll 2
+    for (int x = lane; x < L; x += 32) {
+      const int i = Rr * L + x;
+      double yv[R];
+      float po[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) yv[j] = y[(int64_t)j * n + i];
+      po[0] = G[i];
+      po[1] = p1[q1 + x];
+      if (R == 3) po[R - 1] = p2[i];
+      const double wi = w[i], ci = cdrift[i];
+      double g = 0.0, sp = 0.0;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const float pn = (float)yv[j];
+        if (j == 1) p1[q1 + x] = pn;
+        if (j == 2) p2[i] = pn;
+        const double d = (double)pn - (double)po[j];
+        g += d;
+        sp += (double)pn;
+        acc += d * d;
+      }
+      const double xn = wi - sp;
+      X[i] = (float)xn;
+      const double dc = (xn - g) / (double)R;
+      cdrift[i] = ci + dc;
+      acc += 2.0 * dc * g + (double)R * dc * dc;
+    }
+  }
+  __shared__ double sh[32];
+  const double tot = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = tot;
+}
+
 constexpr int APPLY_TILE = 32;
 constexpr int APPLY_THREADS = 256;  // launch with exactly this many threads
 
@@ -1309,6 +1398,29 @@ int update_exact(pcb_solver* h, double* norm_slot) {
 
 int apply_fast(pcb_solver* h, double* norm_slot) {
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
+  const Fam* F = h->fam;
+  const unsigned all = (1u << h->r) - 1u;
+  const bool two_pass = (h->fmask & all) == all &&
+                        ((h->r == 2 && F[0].kind == K_ROW2 && F[1].kind == K_COL2) ||
+                         (h->r == 3 && F[0].kind == K_X3 && F[1].kind == K_Y3 && F[2].kind == K_Z3));
+  if (two_pass && getenv("PCB_APPLY_TILED") == nullptr) {
+    const int C0 = (int)F[0].C, L = (int)F[0].m;  // rows of L nodes
+    k_apply_rows<<<NODE_GRID, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, C0, L);
+    LAUNCH_CHECK(h);
+    const int n = (int)h->n;
+    const int D1 = h->r == 3 ? (int)h->D.d[1] : 1;
+    const int C1 = h->r == 3 ? (int)(h->D.d[0] * h->D.d[2]) : 0;  // y family: [y][z][x]
+    if (h->r == 2)
+      k_apply_nodes<2><<<g, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, h->cdrift.p, h->X32.p,
+                                                h->w.p, n, L, D1, C1, h->parts.p);
+    else
+      k_apply_nodes<3><<<g, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, h->cdrift.p, h->X32.p,
+                                                h->w.p, n, L, D1, C1, h->parts.p);
+    LAUNCH_CHECK(h);
+    k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, norm_slot, 1);
+    LAUNCH_CHECK(h);
+    return 0;
+  }
   switch (h->r) {
     case 2:
       k_apply_fast<2><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
