@@ -710,9 +710,10 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
 
 // s = y_0 + y_1 + ... (class order), x = w - s, label bits per threshold,
 // partial sums: [unary_t (T)], dual, ww, dd.
-__global__ void k_check_nodes(const double* y, int r, const double* w, int64_t n, int64_t n_own,
-                              int T, const double* thr, uint8_t* bits, double* xcur,
-                              double* parts) {
+__global__ void k_check_nodes(const double* __restrict__ y, int r, const double* __restrict__ w,
+                              int64_t n, int64_t n_own, int T, const double* __restrict__ thr,
+                              uint8_t* __restrict__ bits, double* __restrict__ xcur,
+                              double* __restrict__ parts) {
   double un[MAXT], th[MAXT];  // register arrays: every index below is static
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) {
@@ -770,8 +771,8 @@ struct DirGeom {
 // and direction the edge-array row and the neighbour offset are computed
 // once, and the threads stride along the last axis (coalesced a_e and bits).
 __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_constant__ DirGeom DG,
-                              const __grid_constant__ DirPtrs dw, const uint8_t* bits, int T,
-                              double* parts) {
+                              const __grid_constant__ DirPtrs dw, const uint8_t* __restrict__ bits,
+                              int T, double* __restrict__ parts) {
   double cut[MAXT];
 #pragma unroll
   for (int t = 0; t < MAXT; ++t) cut[t] = 0.0;
