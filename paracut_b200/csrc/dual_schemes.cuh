@@ -138,7 +138,7 @@ int smooth_dual_dev(pcb_solver* h, const double* s, double* slot) {
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   k_smooth_parts<<<g, RED_BLOCK, 0, h->stream>>>(s, h->w.p, h->n, h->parts.p);
   LAUNCH_CHECK(h);
-  k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, 2, h->vals.p + 60);
+  k_reduce_cols<<<1, 32 * 2, 0, h->stream>>>(h->parts.p, g, 2, h->vals.p + 60);
   LAUNCH_CHECK(h);
   k_smooth_final<<<1, 1, 0, h->stream>>>(h->vals.p + 60, slot);
   LAUNCH_CHECK(h);

@@ -258,21 +258,16 @@ __global__ void k_reduce_norm(const double* parts, int64_t count, double* out, i
 
 // vals[j] = sum over blocks b of parts[b * nv + j]; one block, fixed order.
 __global__ void k_reduce_cols(const double* parts, int nblocks, int nv, double* vals) {
-  const int j = threadIdx.x;
+  // one warp per column: lane l sums blocks l, l + 32, ... in order, then a
+  // fixed shuffle tree (deterministic; a single thread per column was load
+  // latency bound, ~55 us per call at 1184 blocks)
+  const int j = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (j >= nv) return;
-  // the same left-to-right sum, with the partials of 16 blocks loaded ahead
-  // of their additions (the loop was load-latency bound)
   double t = 0.0;
-  int b = 0;
-  for (; b + 16 <= nblocks; b += 16) {
-    double v[16];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) v[u] = parts[(int64_t)(b + u) * nv + j];
-#pragma unroll
-    for (int u = 0; u < 16; ++u) t += v[u];
-  }
-  for (; b < nblocks; ++b) t += parts[(int64_t)b * nv + j];
-  vals[j] = t;
+#pragma unroll 8
+  for (int b = lane; b < nblocks; b += 32) t += parts[(int64_t)b * nv + j];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if (lane == 0) vals[j] = t;
 }
 
 // ----------------------------------------------------------------- accessors
@@ -2278,13 +2273,13 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
                                                  h->vals.p + 48,
                                                  h->bits.p, h->xcur.p, h->parts.p);
   LAUNCH_CHECK(h);
-  k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nv, h->vals.p);
+  k_reduce_cols<<<1, 32 * nv, 0, h->stream>>>(h->parts.p, g, nv, h->vals.p);
   LAUNCH_CHECK(h);
   DirPtrs dp{};
   for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
   k_check_edges<<<g, RED_BLOCK, 0, h->stream>>>(h->D, h->DG, dp, h->bits.p, nthr, h->parts.p);
   LAUNCH_CHECK(h);
-  k_reduce_cols<<<1, 32, 0, h->stream>>>(h->parts.p, g, nthr, h->vals.p + 16);
+  k_reduce_cols<<<1, 32 * nthr, 0, h->stream>>>(h->parts.p, g, nthr, h->vals.p + 16);
   LAUNCH_CHECK(h);
   double hv[32];
   CUDA_TRY(hostio::d2h(hv, h->vals.p, 32 * sizeof(double), h->stream));
