@@ -624,7 +624,8 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
     // all loads of the warp's T/NW rows first (memory-level parallelism),
     // then the arithmetic and the stores
     // rows per batch: bounded so the register file holds two blocks per SM
-    // (32-bit node / state indices: pcb_create keeps r * n below 2^31)
+    // (32-bit node indices: pcb_create keeps n below 2^31; family offsets j * n
+    // stay 64-bit)
     constexpr int S = 2;
 #pragma unroll 1
     for (int b0 = 0; b0 < T / NW; b0 += S) {
@@ -649,8 +650,8 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
         } else {
           // COL2 / Z3: family layout == node order; Y3: [y][z][x]
           in[s][j] = ok;
-          qv[s][j] = j * (int)n + (F.kind == K_Y3 ? (Rr % (int)D1) * (int)D0L + (Rr / (int)D1) * (int)L + x : i);
-          po[s][j] = ok ? p[qv[s][j]] : 0.f;
+          qv[s][j] = F.kind == K_Y3 ? (Rr % (int)D1) * (int)D0L + (Rr / (int)D1) * (int)L + x : i;
+          po[s][j] = ok ? p[(int64_t)j * n + qv[s][j]] : 0.f;
         }
       }
       wv[s] = ok ? w[i] : 0.0;
@@ -667,7 +668,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
         if (!in[s][j]) continue;
         const float pn = (float)yv[s][j];
         if (fam_rowlike(FS.f[j].kind)) tile[j][qv[s][j]][lane] = pn;
-        else p[qv[s][j]] = pn;
+        else p[(int64_t)j * n + qv[s][j]] = pn;
         const double d = (double)pn - (double)po[s][j];
         g += d;
         sp += (double)pn;
