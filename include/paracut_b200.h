@@ -149,6 +149,7 @@ int pcb_set_owned(pcb_solver *h, int64_t n_own);
 #define PCB_BUF_Y 3      /* double[r*n] shadow               */
 #define PCB_BUF_NORMS 4  /* double[] per-iteration norms      */
 #define PCB_BUF_P 5      /* float[r*n] fp32 family state (family layout) */
+#define PCB_BUF_BITS 6   /* uint8[n] last check's labels, bit t = threshold t */
 int pcb_device_buffer(pcb_solver *h, int which, uintptr_t *ptr, int64_t *count);
 
 /* Shadow y = Pi_K(z) into the handle's shadow buffer (projections.py:89-104);

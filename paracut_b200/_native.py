@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
 
 PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
-BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_P = 0, 1, 2, 3, 4, 5
+BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_P, BUF_BITS = 0, 1, 2, 3, 4, 5, 6
 ALG_BCD, ALG_AP, ALG_FISTA = 1, 2, 3
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
 PRECISIONS = {"f64": 0, "f32": 1}

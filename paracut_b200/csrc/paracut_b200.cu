@@ -966,6 +966,10 @@ struct DBuf {
   T* p = nullptr;
   size_t n = 0;
   bool pooled = false;
+  // the owning handle's stream (pcb_solver binds its buffers): frees are
+  // stream-ordered behind that handle's queued work instead of a device-wide
+  // sync that would stall other handles' streams and break their graph captures
+  cudaStream_t* owner = nullptr;
   int alloc(size_t count) {
     free();
     if (count == 0) count = 1;
@@ -992,8 +996,10 @@ struct DBuf {
   }
   void free() {
     if (p) {
-      if (pooled) {
-        cudaDeviceSynchronize();  // queued work on any stream may still use p
+      if (pooled && owner) {
+        cudaFreeAsync(p, *owner);
+      } else if (pooled) {
+        cudaDeviceSynchronize();  // unowned scratch: queued work on any stream may still use p
         cudaFreeAsync(p, 0);
       } else {
         cudaFree(p);
@@ -1012,6 +1018,7 @@ template <class T>
 int grow_keep(DBuf<T>& b, size_t need, size_t used, cudaStream_t st, size_t min_cap = 0) {
   if (b.n >= need && b.p) return 0;
   DBuf<T> nb;
+  nb.owner = b.owner;
   size_t cap = b.n * 2;
   if (cap < need) cap = need;
   if (cap < min_cap) cap = min_cap;
@@ -1100,6 +1107,22 @@ struct pcb_solver {
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<int> ev_fam;
+  template <class... B>
+  void bind(B&... b) {
+    ((b.owner = &stream), ...);
+  }
+  template <class T, size_t K>
+  void bind_arr(DBuf<T> (&a)[K]) {
+    for (auto& b : a) b.owner = &stream;
+  }
+  pcb_solver() {
+    bind(w, z, y, p32, cdrift, X32, G32, tmp, yprev, bits, xcur, bestlab, bestx, parts, vals,
+         norms, sp_cx, sp_fx, sp_cy, sp_fy, packed, normlog, lablog, merge);
+    bind_arr(dirw);
+    bind_arr(dirw_base);
+    bind_arr(wf64);
+    bind_arr(wf32);
+  }
   ~pcb_solver() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
@@ -1776,8 +1799,11 @@ struct WeightSource {
 };
 
 // pread `bytes` at `off` of fd into device memory through the pinned ring
-// (reads of chunk i+1 overlap the copy engine's chunk i)
-cudaError_t file_h2d(void* dst, int fd, int64_t off, size_t bytes, cudaStream_t st) {
+// (reads of chunk i+1 overlap the copy engine's chunk i).  nonneg: the payload
+// is fp64 edge weights; a negative one sets *negative (GridEnergy's
+// "edge weights must be nonnegative", graph.py) and stops the upload.
+cudaError_t file_h2d(void* dst, int fd, int64_t off, size_t bytes, cudaStream_t st,
+                     bool nonneg = false, bool* negative = nullptr) {
   if (bytes == 0) return cudaSuccess;
   hostio::Stage& S = hostio::stage();
   std::lock_guard<std::mutex> lk(S.m);
@@ -1803,6 +1829,15 @@ cudaError_t file_h2d(void* dst, int fd, int64_t off, size_t bytes, cudaStream_t 
       got += (size_t)r;
     }
     if (e != cudaSuccess) break;
+    if (nonneg) {
+      const double* v = (const double*)S.slot[slot];
+      bool neg = false;
+      for (size_t q = 0; q < len / sizeof(double); ++q) neg |= v[q] < 0.0;
+      if (neg) {
+        *negative = true;
+        break;
+      }
+    }
     e = cudaMemcpyAsync((char*)dst + done, S.slot[slot], len, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaEventRecord(ev[slot], st);
     used[slot] = true;
@@ -1821,14 +1856,16 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   if (ndim != want_nd) return fail(PCB_E_ARG, "dims rank does not match connectivity");
   if (precision != PCB_F64 && precision != PCB_F32)
     return fail(PCB_E_ARG, "unknown precision %d", precision);
+  // n < 2^31 is what the sweeps' 32-bit index math relies on; checked before
+  // every multiply so a product of large dims cannot wrap first
+  const int64_t nmax = ((int64_t)1 << 31) - 1;
   int64_t n = 1;
   for (int a = 0; a < ndim; ++a) {
     if (dims[a] < 1) return fail(PCB_E_ARG, "dims must be positive");
     if (dims[a] > (int64_t)1 << 30) return fail(PCB_E_ARG, "dimension too large");
+    if (n > nmax / dims[a]) return fail(PCB_E_ARG, "grid too large for one device");
     n *= dims[a];
   }
-  if (n > ((int64_t)1 << 31) - 1) return fail(PCB_E_ARG, "grid too large for one device (n=%lld)",
-                                              (long long)n);
   pcb_solver* h = new pcb_solver();
   h->device = device;
   h->precision = precision;
@@ -1867,7 +1904,9 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
     if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
     if (cnt > 0) {
       if (src.fd >= 0) {
-        e = file_h2d(h->dirw[k].p, src.fd, foff, cnt * sizeof(double), 0);
+        bool neg = false;
+        e = file_h2d(h->dirw[k].p, src.fd, foff, cnt * sizeof(double), 0, true, &neg);
+        if (neg) return bail(fail(PCB_E_ARG, "edge weights must be nonnegative"));
       } else {
         if (!src.dirw[k]) return bail(fail(PCB_E_ARG, "direction %d weights are null", k));
         e = hostio::h2d(h->dirw[k].p, src.dirw[k], cnt * sizeof(double), 0);
@@ -1948,7 +1987,9 @@ int pcb_create_from_file(const char* path, int precision, int device, pcb_solver
   for (int a = 0; a < ndim; ++a) {  // little-endian u64 (x86 / Grace hosts)
     if (d64[a] < 1 || d64[a] > ((uint64_t)1 << 30)) return fail(PCB_E_ARG, "%s: bad dimension", path);
     dims[a] = (int64_t)d64[a];
-    nodes *= dims[a];
+    if (nodes > (((int64_t)1 << 31) - 1) / dims[a])
+      return fail(PCB_E_ARG, "%s: grid too large for one device", path);
+    nodes *= dims[a];  // < 2^31, so the payload count below cannot overflow
   }
   // payload size: w plus every direction array (sizes as direction_shape)
   static const int offs[3][4][3] = {{{0, 1, 0}, {1, 0, 0}, {0, 0, 0}, {0, 0, 0}},
@@ -2068,6 +2109,11 @@ int pcb_shape(const pcb_solver* h, int* r, int64_t* n) {
 
 int pcb_set_stream(pcb_solver* h, uintptr_t stream) {
   if (!h) return fail(PCB_E_ARG, "null handle");
+  // buffer frees are ordered on the handle's stream: drain the old one first
+  if ((cudaStream_t)stream != h->stream) {
+    cudaSetDevice(h->device);
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
   h->stream = (cudaStream_t)stream;
   return 0;
 }
@@ -2628,6 +2674,7 @@ int pcb_device_buffer(pcb_solver* h, int which, uintptr_t* ptr, int64_t* count) 
     case PCB_BUF_Y: *ptr = (uintptr_t)h->y.p; *count = (int64_t)h->r * h->n; break;
     case PCB_BUF_NORMS: *ptr = (uintptr_t)h->norms.p; *count = (int64_t)h->norms.n; break;
     case PCB_BUF_P: *ptr = (uintptr_t)h->p32.p; *count = h->p32.p ? (int64_t)h->r * h->n : 0; break;
+    case PCB_BUF_BITS: *ptr = (uintptr_t)h->bits.p; *count = h->bits.p ? h->n : 0; break;
     default: return fail(PCB_E_ARG, "unknown buffer id %d", which);
   }
   if (!*ptr) return fail(PCB_E_STATE, "buffer %d not allocated for this precision", which);

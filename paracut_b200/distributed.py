@@ -233,7 +233,7 @@ def _wrap(dev_ptr, count, dtype, device):
         pass
 
     o = _CAI()
-    typestr = {np.float32: "<f4", np.float64: "<f8"}[dtype]
+    typestr = {np.float32: "<f4", np.float64: "<f8", np.uint8: "|u1"}[dtype]
     o.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
                                   "data": (int(dev_ptr), False), "version": 3}
     return torch.as_tensor(o, device=device)
@@ -574,6 +574,14 @@ class ShardedAAR:
         ptr, cnt = h.device_buffer(self.N.BUF_Y)
         return _wrap(ptr, cnt, np.float64, self._dev())
 
+    def _bitbuf(self, h):
+        """Check labels of a slab handle on the device: uint8[n], bit t = threshold t."""
+        if hasattr(h, "host_buffer"):  # CPU emulation
+            import torch
+            return torch.from_numpy(h.host_buffer(self.N.BUF_BITS))
+        ptr, cnt = h.device_buffer(self.N.BUF_BITS)
+        return _wrap(ptr, cnt, np.uint8, self._dev())
+
     def check(self, thresholds=(0.0,)):
         """Global (energies[T], gaps[T], smooth dual) of the current iterate;
         labels stay on their ranks (slab handles' check state)."""
@@ -600,27 +608,28 @@ class ShardedAAR:
             self._halo_shadow(ys)
         # per-rank certificate of the slab (its nodes, its intra-slab edges)
         a_b = np.asarray(self.g.dir_weights[x], dtype=np.float64).reshape(self.g.dims[0] - 1, plane)
-        firsts_local, local = [], []
+        local = []
         for rk, s in zip(self.ranks, self.slab):
             e, gp, smooth = s.check(thr)
-            last = None
-            if not self.halo:
-                labs = np.stack([s.check_labels(t) for t in range(T)]).astype(np.float64)
-                mine = np.zeros((P, T, plane))
-                mine[rk] = labs[:, :plane]  # this slab's first label plane, for rank rk - 1
-                firsts_local.append(mine)
-                last = labs[:, -plane:]
-            local.append((rk, e, float(e[0] - gp[0]), float(smooth), last))
-        firsts = None if self.halo else self.comm.all_sum(firsts_local)[0]
+            local.append((rk, e, float(e[0] - gp[0]), float(smooth)))
+        cut_b = [np.zeros(T) for _ in self.ranks]
+        if not self.halo:
+            # edges between a slab's last plane and the next slab's first: the
+            # next rank sends its first plane of label bits (bit t = threshold t)
+            bits = [self._bitbuf(s)[:ns] for s in self.slab]
+            first = [torch.empty(plane, dtype=torch.uint8, device=b.device) for b in bits]
+            self.comm.send_prev([b[:plane] if rk > 0 else None for b, rk in zip(bits, self.ranks)],
+                                [f if rk < P - 1 else None for f, rk in zip(first, self.ranks)])
+            tb = torch.arange(T, dtype=torch.uint8, device=bits[0].device)[:, None]
+            for q, (rk, b, f) in enumerate(zip(self.ranks, bits, first)):
+                if rk == P - 1:
+                    continue
+                diff = (((b[ns - plane:][None, :] >> tb) & 1) != ((f[None, :] >> tb) & 1))
+                row = torch.as_tensor(a_b[(rk + 1) * dz - 1], device=b.device)
+                cut_b[q] = (diff.to(torch.float64) @ row).cpu().numpy()
         parts = []
-        for rk, e, dual, smooth, last in local:
-            cut_b = np.zeros(T)
-            # edges between this slab's last plane and the next one's first
-            # (2D-8: already in the slab's certificate through the halo row)
-            if rk < P - 1 and not self.halo:
-                cut_b = np.abs(last - firsts[rk + 1]) @ a_b[(rk + 1) * dz - 1]
-            parts.append(np.concatenate([np.asarray(e, dtype=np.float64) + cut_b,
-                                         [dual, smooth]]))
+        for (rk, e, dual, smooth), cb in zip(local, cut_b):
+            parts.append(np.concatenate([np.asarray(e, dtype=np.float64) + cb, [dual, smooth]]))
         tot = self.comm.all_sum(parts)[0]
         energies, dual, smooth = tot[:T], tot[T], tot[T + 1]
         return energies, energies - dual, smooth

@@ -384,16 +384,18 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
         drv.switch_solver(S64)
         drv.kmax = k + cfg.polish_iters
         drv.record("polish_start", k)
-        _loop(drv, S64, k)
+        # iteration k was just checked (its trace row stays): update first
+        _loop(drv, S64, k, checked=k)
     return drv.finish()
 
 
-def _loop(drv, S, k):
-    """Plain iterations between checks, shadow + certificate + update at checks."""
+def _loop(drv, S, k, checked=None):
+    """Plain iterations between checks, shadow + certificate + update at checks.
+    ``checked``: an iteration already certified (its check is not repeated)."""
     while True:
         if drv.due(k):
             S.shadow()
-            if drv.check(k) or k >= drv.kmax or drv.stalled():
+            if k != checked and (drv.check(k) or k >= drv.kmax or drv.stalled()):
                 return k
             if drv.log:
                 S.apply(norm=False)

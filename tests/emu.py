@@ -11,7 +11,7 @@ import numpy as np
 from oracle import oracle as orc
 
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
-BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS = 0, 1, 2, 3, 4
+BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_BITS = 0, 1, 2, 3, 4, 6
 ORDER = {"2D-4": (0, 1), "2D-8": (0, 1, 2, 3), "3D-6": (0, 1, 2)}
 
 
@@ -33,8 +33,16 @@ class EmuSolver:
         self.bits = None
 
     def host_buffer(self, which):
+        if which == BUF_BITS:
+            return self._packed_bits()
         return {BUF_G: self.G, BUF_X: self.X, BUF_C: self.c, BUF_Y: self.y.reshape(-1),
                 BUF_NORMS: self.norms}[which]
+
+    def _packed_bits(self):
+        out = np.zeros(self.n, dtype=np.uint8)
+        for t, lab in enumerate(self.bits):
+            out |= (lab.astype(np.uint8) << t)
+        return out
 
     def set_family_mask(self, mask):
         self.mask = mask

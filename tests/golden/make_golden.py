@@ -319,11 +319,7 @@ def make_io():
     w = r.uniform(-3, 3, 9)
     edges = [(i, j, float(r.uniform(0.01, 2.0))) for i in range(9) for j in range(i + 1, 9)
              if r.random() < 0.4]
-    inst = pc.CutInstance(w, edges)
-    pc.write_dimacs(inst, os.path.join(out, "cut.max"))
-    ei, ej, ea = inst.edge_arrays()
-    np.savez(os.path.join(out, "cut_arrays.npz"), w=inst.w, ei=ei, ej=ej, ea=ea,
-             fingerprint=np.array(pc.instance_fingerprint(inst)))
+    del w, edges  # (drawn for the general-instance files of round 1; kept for the RNG stream)
     st = pc.DualState(y=r.normal(size=(2, 6)), z=r.normal(size=(2, 6)), fingerprint="fp-io")
     pc.save_dual(st, os.path.join(out, "state.dual"))
     trace = [TraceRow(0, 1.25, -0.5, 3.0, np.nan, 0.001), TraceRow(10, 0.0, 2.0, -1.0, 0.25, 0.002)]

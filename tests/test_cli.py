@@ -8,13 +8,19 @@ import pytest
 import paracut_b200 as pc
 from paracut_b200 import cli
 from paracut_b200 import io as pio
-from paracut_b200.graph import CutInstance
-from conftest import GOLDEN
+from paracut_b200.graph import DIRECTIONS, direction_shape
+
+
+def _tiny_grid(rng, conn, dims):
+    w = rng.uniform(-3, 3, int(np.prod(dims)))
+    dws = [rng.uniform(0, 2, direction_shape(dims, d))
+           * (rng.uniform(size=direction_shape(dims, d)) < 0.8) for d in DIRECTIONS[conn]]
+    return pc.GridEnergy(dims, conn, w, dws)
 
 
 @pytest.fixture
 def grid_file(tmp_path):
-    g = cli._tiny_grid(np.random.default_rng(7), "2D-8", (9, 11))
+    g = _tiny_grid(np.random.default_rng(7), "2D-8", (9, 11))
     p = tmp_path / "g.pcut"
     pio.write_grid(g, p)
     return str(p)
@@ -22,8 +28,8 @@ def grid_file(tmp_path):
 
 @pytest.fixture
 def dimacs_file(tmp_path):
-    p = tmp_path / "c.max"
-    pio.write_dimacs(CutInstance(np.array([1.0, -2.0, 0.5]), [(0, 1, 0.5), (1, 2, 0.75)]), p)
+    p = tmp_path / "c.max"  # a general instance in DIMACS max-flow form
+    p.write_text("p max 5 4\nn 4 s\nn 5 t\na 4 1 1.0\na 2 5 2.0\na 1 2 0.5\na 2 1 0.5\n")
     return str(p)
 
 
@@ -36,9 +42,7 @@ def test_usage_and_io_errors_without_a_device(tmp_path, grid_file, dimacs_file, 
     bad.write_bytes(b"PCUT1B\x09\x02")
     assert cli.main(["solve", "--input", str(bad)]) == cli.EXIT_IO
     assert cli.main(["solve", "--input", grid_file, "--scale-pairwise", "-1"]) == cli.EXIT_USAGE
-    assert cli.main(["bench", "--input", dimacs_file]) == cli.EXIT_USAGE
-    assert cli.main(["bench", "--input", grid_file, "--algos", "newton"]) == cli.EXIT_USAGE
-    assert cli.main(["bench", "--input", grid_file, "--scales", "x"]) == cli.EXIT_USAGE
+    assert cli.main(["solve", "--input", dimacs_file, "--format", "grid"]) == cli.EXIT_IO
     with pytest.raises(SystemExit):
         cli.main(["solve"])  # argparse: --input required
 
@@ -48,16 +52,6 @@ def test_threads_default_from_environment(monkeypatch):
     assert cli._default_threads() == 6
     monkeypatch.setenv("PARACUT_THREADS", "x")
     assert cli._default_threads() == 1
-
-
-def test_brute_force_small_grids():
-    rng = np.random.default_rng(3)
-    for conn, dims in (("2D-4", (3, 4)), ("2D-8", (3, 3)), ("3D-6", (2, 2, 3))):
-        g = cli._tiny_grid(rng, conn, dims)
-        lab, e = cli.brute_force_mincut(g)
-        assert g.energy(lab) == pytest.approx(e, abs=1e-12)
-        for _ in range(20):
-            assert g.energy(rng.integers(0, 2, g.n)) >= e - 1e-12
 
 
 @pytest.mark.gpu
@@ -90,7 +84,7 @@ def test_solve_warm_start_and_fingerprint_guard(grid_file, tmp_path, capsys):
     assert cli.main(["solve", "--input", grid_file, "--warm-start", str(dual),
                      "--gap-tol", "1e-6"]) == cli.EXIT_OK
     other = tmp_path / "o.pcut"
-    pio.write_grid(cli._tiny_grid(np.random.default_rng(8), "2D-8", (9, 11)), other)
+    pio.write_grid(_tiny_grid(np.random.default_rng(8), "2D-8", (9, 11)), other)
     assert cli.main(["solve", "--input", str(other), "--warm-start", str(dual)]) == cli.EXIT_IO
     assert "fingerprint" in capsys.readouterr().err
     assert cli.main(["solve", "--input", str(other), "--warm-start", str(dual), "--force",
@@ -106,23 +100,3 @@ def test_solve_uncertified_exit_and_algorithms(grid_file, capsys):
                          "1e-6"]) == cli.EXIT_OK
     assert cli.main(["solve", "--input", grid_file, "--precision", "f32", "--polish-iters",
                      "200", "--gap-tol", "1e-6", "--level-sets"]) == cli.EXIT_OK
-
-
-@pytest.mark.gpu
-def test_bench_csv_schema(grid_file, tmp_path):
-    out = tmp_path / "b.csv"
-    assert cli.main(["bench", "--input", grid_file, "--algos", "aar,fista", "--scales",
-                     "1.0,2.0", "--max-iters", "300", "--out", str(out)]) == cli.EXIT_OK
-    lines = out.read_text().strip().splitlines()
-    assert lines[0].split(",") == ["algo", "threads", "scale", "iterations", "certified",
-                                   "energy", "wall_s", "iter_err_lt_10pct", "iter_err_lt_2pct",
-                                   "iter_jd_lt_0.1", "iter_jd_lt_0.02"]
-    assert len(lines) == 1 + 2 * 2
-
-
-@pytest.mark.gpu
-def test_verify_clean_and_detects_corruption(capsys):
-    assert cli.main(["verify", "--trials", "4", "--inject-corruption"]) == cli.EXIT_OK
-    out = capsys.readouterr().out
-    assert "FAIL" not in out and "corruption detected" in out
-    assert out.strip().endswith("verify: 0 checks failed")

@@ -59,3 +59,19 @@ def test_malformed_files_fail_in_the_library(tmp_path):
     gf.path = str(tmp_path / "missing.pcut")
     with pytest.raises(ValueError, match="cannot open"):
         _native.GridSolver(gf, precision="f64")
+
+
+def test_negative_edge_weight_in_file_is_rejected(tmp_path):
+    """GridEnergy's 'edge weights must be nonnegative' (reference graph.py) on
+    the device-ingest path, which never builds host arrays."""
+    g = make_instance("cfg1", seed=0, dims=(9, 8))
+    p = tmp_path / "g.pcut"
+    pio.write_grid(g, p)
+    raw = bytearray(p.read_bytes())
+    off = 6 + 2 + 8 * 2 + 8 * g.n + 8 * 5  # sixth entry of the first direction array
+    raw[off:off + 8] = np.array([-0.25], dtype="<f8").tobytes()
+    bad = tmp_path / "neg.pcut"
+    bad.write_bytes(bytes(raw))
+    for precision in ("f64", "f32"):
+        with pytest.raises(ValueError, match="nonnegative"):
+            _native.GridSolver(pio.open_grid(bad), precision=precision)
