@@ -42,7 +42,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "grid-node TV-prox updates/sec per AAR iteration"
-CPU_SAMPLE_NODES = 1 << 22
 
 
 def parse_args():
@@ -135,37 +134,45 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
-def crop_axis0(g, nodes_cap):
-    """Slab of the instance along the slowest axis with <= nodes_cap nodes."""
-    from paracut_b200.graph import GridEnergy, DIRECTIONS
-    dims = tuple(g.dims)
-    plane = int(np.prod(dims[1:]))
-    rows = max(2, min(dims[0], nodes_cap // plane))
-    if rows >= dims[0]:
-        return g
-    nd = (rows,) + dims[1:]
-    w = g.w.reshape(dims)[:rows].ravel()
-    dws = []
-    for d, a in zip(DIRECTIONS[g.connectivity], g.dir_weights):
-        dws.append(np.ascontiguousarray(a[:rows - abs(d[0])]))
-    return GridEnergy(nd, g.connectivity, np.ascontiguousarray(w), dws)
-
-
-def cpu_port_rate(g, iters, warm=1):
-    """(updates/s, threads, sample) for the oracle's C port of the reference loop."""
+def cpu_port_rate(g, iters, threads, warm=1, runner=None):
+    """(updates/s, seconds per iteration) of the oracle's C port of the
+    reference loop (bitwise the reference's fp64 arithmetic, OpenMP over
+    chains) on the whole workload instance with `threads` host threads."""
     from oracle import oracle as orc
-    sample = crop_axis0(g, CPU_SAMPLE_NODES)
-    threads = orc.max_threads()
-    run = orc.AARRunner(sample, threads=threads)
-    run.run(warm, final_shadow=False)
+    run = runner if runner is not None else orc.AARRunner(g, threads=threads)
+    run.threads = int(threads)
+    if warm:
+        run.run(warm, final_shadow=False)
     t0 = time.perf_counter()
     run.run(iters, final_shadow=False)
     dt = time.perf_counter() - t0
-    rate = run.r * run.n * iters / dt
-    desc = ("%s slab %s of the workload instance, %d AAR iterations (fp64, bitwise the "
-            "reference's arithmetic), oracle/paracut_oracle.c OpenMP over chains"
-            % (g.connectivity, "x".join(map(str, sample.dims)), iters))
-    return rate, threads, desc, dt
+    return run.r * run.n * iters / dt, dt / iters, run
+
+
+def cpu_baseline(g, workload, iters_all=3, iters_one=1, ttc_iters=None):
+    """The reference arithmetic on this box's host cores, same instance as the
+    GPU line: all cores and one core, plus the CPU time to a certified cut
+    extrapolated from the per-iteration time (the GPU solve's iteration count
+    to its certificate; checks every 10 iterations not counted)."""
+    from oracle import oracle as orc
+    tmax = orc.max_threads()
+    rate, spi, run = cpu_port_rate(g, iters_all, tmax)
+    rate1, spi1, _ = cpu_port_rate(g, iters_one, 1, warm=0, runner=run)
+    out = {"value": rate, "unit": "updates/s", "cores": tmax, "kind": "port",
+           "sample": ("%s %s (the whole %s instance), %d AAR iterations on %d threads and %d on "
+                      "1 thread after one warm-up iteration; oracle/paracut_oracle.c: the "
+                      "reference loop in its fp64 operation order, OpenMP over chains"
+                      % (g.connectivity, "x".join(map(str, g.dims)), workload, iters_all, tmax,
+                         iters_one)),
+           "s_per_iter": spi, "one_core": {"value": rate1, "unit": "updates/s", "cores": 1,
+                                           "s_per_iter": spi1}}
+    if ttc_iters:
+        out["time_to_cut"] = {"value": spi * ttc_iters, "unit": "s", "cores": tmax,
+                              "iterations": int(ttc_iters), "extrapolated": True,
+                              "one_core_value": spi1 * ttc_iters,
+                              "rule": "per-iteration time x the GPU solve's iterations to its "
+                                      "certificate (check iterations not counted)"}
+    return out
 
 
 def dist_setup(args):
@@ -176,29 +183,33 @@ def dist_setup(args):
 
 
 def run_reference(args, world, rank):
+    """The reference's CPU implementation of the path (its loop in the
+    reference's fp64 operation order: oracle/paracut_oracle.c) on the box's
+    host cores, on the SAME workload instance as our arm; rank 0 only."""
     from paracut_b200.instances import CONFIGS, make_instance
     if rank != 0:
         return
+    from oracle import oracle as orc
     spec = CONFIGS[args.workload]
     g = make_instance(spec, seed=args.seed)
-    from oracle import oracle as orc
-    sample = crop_axis0(g, CPU_SAMPLE_NODES)
     threads = orc.max_threads()
-    run = orc.AARRunner(sample, threads=threads)
+    run = orc.AARRunner(g, threads=threads)
     run.run(max(args.warmup, 1), final_shadow=False)
     t0 = time.perf_counter()
     run.run(args.steps, final_shadow=False)
     dt = time.perf_counter() - t0
     value = run.r * run.n * args.steps / dt
-    desc = ("%s slab %s of the %s instance (seed %d), fp64; each step one AAR iteration"
-            % (g.connectivity, "x".join(map(str, sample.dims)), args.workload, args.seed))
+    desc = ("%s %s, the whole %s instance (seed %d), fp64 (the reference is fp64-only); each "
+            "step one AAR iteration on %d threads" % (g.connectivity, "x".join(map(str, g.dims)),
+                                                      args.workload, args.seed, threads))
     line = {
         "metric": METRIC, "value": value, "unit": "updates/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json generator)",
         "config": {"workload": args.workload, "dims": list(spec.dims),
-                   "connectivity": spec.connectivity, "sample_dims": list(sample.dims)},
+                   "connectivity": spec.connectivity, "r": run.r, "n": run.n,
+                   "step": "1 AAR iteration"},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port",
                          "sample": desc},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
@@ -411,12 +422,6 @@ def main():
             "iteration_achieved_gbs": B_iter * args.steps / (ms / 1e3) / 1e9,
             "iteration_bytes": B_iter}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        rate, threads, desc, _ = cpu_port_rate(g, args.cpu_iters)
-        cpu = {"value": rate, "unit": "updates/s", "cores": threads, "kind": "port",
-               "sample": desc}
-
     e2e = None
     if not args.no_e2e:
         S.close()
@@ -449,6 +454,11 @@ def main():
     ttc = None
     if rank == 0 and world == 1 and not args.no_ttc:
         ttc = time_to_cut(pc, g, precision, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(g, args.workload, iters_all=args.cpu_iters,
+                           ttc_iters=ttc["iterations"] if ttc else None)
 
     if rank == 0:
         line = {

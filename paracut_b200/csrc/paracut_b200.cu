@@ -2110,9 +2110,15 @@ int pcb_shape(const pcb_solver* h, int* r, int64_t* n) {
 int pcb_set_stream(pcb_solver* h, uintptr_t stream) {
   if (!h) return fail(PCB_E_ARG, "null handle");
   // buffer frees are ordered on the handle's stream: drain the old one first
+  // (not while either stream is being captured into a graph: a sync would
+  // invalidate the capture, and captured work is not queued work)
   if ((cudaStream_t)stream != h->stream) {
     cudaSetDevice(h->device);
-    CUDA_TRY(cudaStreamSynchronize(h->stream));
+    cudaStreamCaptureStatus c_old = cudaStreamCaptureStatusNone, c_new = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(h->stream, &c_old));
+    CUDA_TRY(cudaStreamIsCapturing((cudaStream_t)stream, &c_new));
+    if (c_old == cudaStreamCaptureStatusNone && c_new == cudaStreamCaptureStatusNone)
+      CUDA_TRY(cudaStreamSynchronize(h->stream));
   }
   h->stream = (cudaStream_t)stream;
   return 0;

@@ -158,13 +158,12 @@ def test_bench_helpers():
     bench = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(bench)
     g = make_instance("cfg4", seed=0, dims=(40, 30, 20))
-    s = bench.crop_axis0(g, 30 * 20 * 7)
-    assert s.dims == (7, 30, 20)
-    assert np.array_equal(s.w, g.w.reshape(g.dims)[:7].ravel())
-    assert s.dir_weights[2].shape == (6, 30, 20)
     g8 = make_instance("cfg3", seed=0, dims=(20, 30))
     fe = bench._family_edges(g8)
     assert sum(fe) == sum(int(np.count_nonzero(a)) for a in g8.dir_weights)
-    # the CPU port leg runs and reports a positive rate
-    rate, threads, desc, dt = bench.cpu_port_rate(make_instance("cfg4", seed=0, dims=(8, 16, 16)), 2)
-    assert rate > 0 and threads >= 1 and "slab" in desc
+    # the CPU leg runs on the whole instance at all cores and one core
+    cb = bench.cpu_baseline(make_instance("cfg4", seed=0, dims=(8, 16, 16)), "cfg4", 2, 1,
+                            ttc_iters=100)
+    assert cb["value"] > 0 and cb["cores"] >= 1 and cb["one_core"]["cores"] == 1
+    assert "8x16x16" in cb["sample"] and cb["time_to_cut"]["extrapolated"]
+    assert cb["time_to_cut"]["value"] == pytest.approx(cb["s_per_iter"] * 100)
