@@ -143,6 +143,15 @@ int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
  * and pcb_apply_g leaves their norm term out.  n_own = n: no halo. */
 int pcb_set_owned(pcb_solver *h, int64_t n_own);
 /* Device pointer and element count of a handle buffer (for collectives). */
+/* Verified sweeps of the double-buffered fp32 step:
+ * per family (r entries each, NULL allowed) the current mode (1 = the next
+ * plain iteration verifies last iteration's segmentation, 0 = taut-string
+ * scan, -1 = family always scans), how many sweeps ran verified so far and
+ * how many chains those repaired locally, how many ran as scans and in how
+ * many chains those changed the segmentation.  Diagnostics; syncs the stream. */
+int pcb_verify_stats(pcb_solver* h, int* modes, int64_t* sweeps, int64_t* repaired,
+                     int64_t* scans, int64_t* changed);
+
 #define PCB_BUF_G 0      /* float[n] accumulator / exported g */
 #define PCB_BUF_X 1      /* float[n] primal                  */
 #define PCB_BUF_C 2      /* double[n] drift                  */

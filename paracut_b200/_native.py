@@ -74,6 +74,7 @@ def _declare(L):
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
     L.pcb_set_profiling.argtypes = [P, INT]
     L.pcb_profile_read.argtypes = [P, P, P]
+    L.pcb_verify_stats.argtypes = [P, P, P, P, P, P]
     L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
     L.pcb_set_owned.argtypes = [P, I64]
     L.pcb_log_start.argtypes = [P]
@@ -96,7 +97,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
-           "pcb_log_jaccard")
+           "pcb_log_jaccard", "pcb_verify_stats")
 
 
 def lib():
@@ -419,6 +420,14 @@ class GridSolver:
 
     def set_profiling(self, on):
         check(lib().pcb_set_profiling(self.handle, int(bool(on))))
+
+    def verify_stats(self, scans=False):
+        """(modes, verified sweeps, repaired chains[, scan sweeps, changed
+        chains]) per family (pcb_verify_stats)."""
+        modes = np.zeros(self.r, dtype=np.int32)
+        out = [np.zeros(self.r, dtype=np.int64) for _ in range(4)]
+        check(lib().pcb_verify_stats(self.handle, ptr(modes), *[ptr(a) for a in out]))
+        return (modes, *out) if scans else (modes, out[0], out[1])
 
     def profile_read(self):
         ms = np.zeros(self.r)

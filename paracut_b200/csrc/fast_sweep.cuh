@@ -81,7 +81,28 @@ struct Args {
   const int* merge;
   int nb;
   int export_g;     // LAST: also store the per-node g = sum_j d_j (fp32) in G
+  // Double-buffered step (nullptr: in place).  The sweep reads p, c, X and
+  // Gi and writes po, co, Xo and G, so its inputs stay intact for the local
+  // repair of a verified sweep (VER) and for any other reader of the step.
+  float* po;        // new family state
+  double* co;       // LAST: new drift
+  float* Xo;        // LAST: new primal
+  const float* Gi;  // MID / LAST: accumulator in (G is the accumulator out)
+  // Segment hints (SCAN writes, VER reads): per tile of TP positions one
+  // uint16 per chain, [tile][C]; bit q: the left boundary of position
+  // tile*TP+q is a ceiling touch (x rises), bit 8+q: a floor touch (x falls).
+  uint16_t* sg;
+  const int* vmode; // device mode word of this family: 1 = VER sweeps, else SCAN
+  int* vcount;      // SCAN: chains whose hints changed; VER: chains repaired
 };
+
+// in-place defaults for the double-buffer fields
+inline void args_inplace(Args& a) {
+  if (!a.po) a.po = a.p;
+  if (!a.co) a.co = a.c;
+  if (!a.Xo) a.Xo = a.X;
+  if (!a.Gi) a.Gi = a.G;
+}
 
 // TMA descriptors of one family launch.  Strided families (cols, 3D y / z)
 // whose warps' 32 chains are 32 consecutive nodes at every position load
@@ -225,28 +246,231 @@ __device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t 
   const float p32 = (float)pn;
   const double d = (double)p32 - (double)pold;
   double nrm = nrm_d(d, 0.0);
-  A.p[fi] = p32;
+  A.po[fi] = p32;
   if (ROLE == FIRST) {
     A.G[nd] = (float)d;
   } else if (ROLE == MID) {
-    A.G[nd] = (float)((double)A.G[nd] + d);
+    A.G[nd] = (float)((double)A.Gi[nd] + d);
   } else {
-    const float g32 = (float)((double)A.G[nd] + d);
+    const float g32 = (float)((double)A.Gi[nd] + d);
     const double g = (double)g32;
     const double xn = (double)A.X[nd] - g;
-    A.X[nd] = (float)xn;
+    A.Xo[nd] = (float)xn;
     const double dcv = (xn - g) * A.inv_r;
-    A.c[nd] = cz + dcv;
+    A.co[nd] = cz + dcv;
     if (A.export_g) A.G[nd] = g32;
     nrm = nrm_last(dcv, g, A.rd, nrm);
   }
   return nrm;
 }
 
+struct Spec {
+  int i0, pe, k, c0x, f0x;
+  double t, skr, cs, fs, Lc, Lf;
+  bool fresh;
+};
+
+template <class ZA>
+__device__ __forceinline__ void spec_next_bend(Spec& S, int m, const ZA& za, int* bk_out,
+                                               int* bt_out, double* xv_out = nullptr) {
+  for (;;) {
+    const int kp = S.k;
+    double zabs, av;
+    za(kp, &zabs, &av);
+    S.k = kp + 1;
+    if (S.fresh) {
+      S.t = zabs;
+      S.fresh = false;
+    }
+    S.skr += zabs - S.t;
+    const bool inner = S.k < m;
+    const double rk = inner ? av : 0.0;
+    if (inner && av == 0.0) S.pe = S.k;
+    const double inv = rcp_r<double>(S.k - S.i0);
+    S.Lc += S.cs;
+    S.Lf += S.fs;
+    const double u = S.skr + rk;
+    if (S.c0x < 0 || u <= S.Lc) {
+      S.c0x = S.k;
+      S.cs = u * inv;
+      S.Lc = u;
+    }
+    int bk = -1, bt = 0;
+    double fill = 0.0;
+    if (S.f0x >= 0 && S.cs < S.fs) {
+      bk = S.f0x; bt = -1; fill = S.fs;
+    } else {
+      const double l = S.skr - rk;
+      if (S.f0x < 0 || l >= S.Lf) {
+        S.f0x = S.k;
+        S.fs = l * inv;
+        S.Lf = l;
+      }
+      if (S.fs > S.cs) {
+        bk = S.c0x; bt = 1; fill = S.cs;
+      } else if (S.k == S.pe) {
+        if (S.c0x != S.pe && S.Lc < S.skr) {
+          bk = S.c0x; bt = 1; fill = S.cs;
+        } else if (S.f0x != S.pe && S.Lf > S.skr) {
+          bk = S.f0x; bt = -1; fill = S.fs;
+        } else {
+          bk = S.pe; bt = 0; fill = S.skr * inv;
+        }
+      }
+    }
+    if (bk >= 0) {
+      if (xv_out) *xv_out = S.t + fill;  // the closed segment's prox value
+      double ab = 0.0;
+      if (bt != 0) {
+        double dz;
+        za(bk - 1, &dz, &ab);
+      }
+      const bool piece_end = bk == S.pe;
+      S.i0 = S.k = bk;
+      S.fresh = true;
+      S.skr = piece_end ? 0.0 : -(double)bt * ab;
+      if (piece_end) S.pe = m;
+      S.c0x = S.f0x = -1;
+      S.cs = S.fs = S.Lc = S.Lf = 0.0;
+      *bk_out = bk;
+      *bt_out = piece_end ? 0 : bt;
+      return;
+    }
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Local repair of a verified chain whose candidate failed somewhere in
+// [ff, fl] (VER sweep; everything from global memory, inputs intact in the
+// double-buffered step).  The true string is localised between two points:
+//  * q_L <= ff: the first common bend of the two strings anchored at the
+//    floor and at the ceiling of a gate g < ff (taut strings to a common end
+//    never cross, so the true one passes there too -- the merge-point argument
+//    of k_merge), accepted if the candidate has the same touch there (then the
+//    candidate before q_L, which passed every check, is the true solution);
+//    g moves back until that holds (g = 0, the chain start, always does);
+//  * the taut string from q_L is exact; it is emitted bend by bend until a
+//    bend past fl where the candidate has the same touch -- from there on the
+//    candidate (checked, with a true left dual) is the true solution.
+// The emitted range replaces what the sweep wrote; the step-norm partial is
+// corrected by the difference.  Hints of the range are rewritten.
 template <int ROLE, bool ROWLIKE>
+__device__ __noinline__ double repair_lane(const Args& A, int c32, int base32, int ff, int fl,
+                                           int emit_hi) {
+  const Fam& F = A.F;
+  const int m = F.m, C32 = (int)F.C;
+  const int ns32 = (int)F.ns, zz32 = (int)F.zz, ph32 = F.phase;
+  auto node = [&](int pos) {
+    return ROWLIKE ? base32 + pos * ns32 + zz32 * ((pos + ph32) & 1) : base32 + pos * ns32;
+  };
+  auto za = [&](int pos, double* z, double* a) {
+    const int fi = pos * C32 + c32;
+    *z = (double)A.p[fi] + A.c[node(pos)];
+    *a = pos < m - 1 ? (double)A.wf[fi] : 0.0;
+  };
+  auto cand = [&](int e) {  // hinted side of edge e (+1 ceiling, -1 floor, 0 none)
+    const unsigned w = A.sg[(e / TP) * C32 + c32];
+    const int q = e % TP;
+    return (int)((w >> q) & 1u) - (int)((w >> (8 + q)) & 1u);
+  };
+  // 1. q_L
+  int qL = 0, qt = 0;
+  for (int delta = 4;; delta *= 2) {
+    const int g = ff - delta;
+    if (g <= 0) break;
+    const double ag = (double)A.wf[(g - 1) * C32 + c32];
+    if (ag == 0.0) {  // a piece start: a true point for every string
+      qL = g;
+      break;
+    }
+    Spec Fs{g, m, g, -1, -1, 0.0, ag, 0.0, 0.0, 0.0, 0.0, true};
+    Spec Us{g, m, g, -1, -1, 0.0, -ag, 0.0, 0.0, 0.0, 0.0, true};
+    int pf, tf, pu, tu;
+    spec_next_bend(Fs, m, za, &pf, &tf);
+    spec_next_bend(Us, m, za, &pu, &tu);
+    int q = -1, t = 0;
+    for (;;) {
+      if (pf == pu && tf == tu) {
+        q = pf;
+        t = tf;
+        break;
+      }
+      if (min(pf, pu) > ff) break;
+      if (pf <= pu) spec_next_bend(Fs, m, za, &pf, &tf);
+      else spec_next_bend(Us, m, za, &pu, &tu);
+    }
+    if (q >= 0 && q <= ff && (t == 0 || cand(q - 1) == t)) {
+      qL = q;
+      qt = t;
+      break;
+    }
+  }
+  // 2. the exact string from q_L
+  double nrm = 0.0;
+  const double a0 = (qL > 0 && qt != 0) ? (double)A.wf[(qL - 1) * C32 + c32] : 0.0;
+  Spec S{qL, m, qL, -1, -1, 0.0, -(double)qt * a0, 0.0, 0.0, 0.0, 0.0, true};
+  int s0 = qL;
+  for (;;) {
+    int bk, bt;
+    double xv;
+    spec_next_bend(S, m, za, &bk, &bt, &xv);
+    const bool stop = bk >= m || (bk - 1 > fl && (bt == 0 || cand(bk - 1) == bt));
+    for (int j = s0; j < bk; ++j) {
+      const int fi = j * C32 + c32, nd = node(j);
+      const float pin = A.p[fi];
+      const double cz = A.c[nd];
+      const float p32 = (float)(((double)pin + cz) - xv);
+      const double d = (double)p32 - (double)pin;
+      double r = d * d;
+      // the sweep emitted (and counted) this position: below emit_hi, or (the
+      // lean sweep, emit_hi < 0) wherever it did not leave a NaN hole
+      const bool was = emit_hi >= 0 ? j < emit_hi : !isnan(A.po[fi]);
+      const double dw = was ? (double)A.po[fi] - (double)pin : 0.0;
+      if (was) r -= dw * dw;
+      A.po[fi] = p32;
+      if (ROLE == FIRST) {
+        A.G[nd] = (float)d;
+      } else if (ROLE == MID) {
+        A.G[nd] = (float)((double)A.Gi[nd] + d);
+      } else {
+        const double gi = (double)A.Gi[nd], xi = (double)A.X[nd];
+        const double g = (double)(float)(gi + d);
+        const double xn = xi - g;
+        A.Xo[nd] = (float)xn;
+        const double dcv = (xn - g) * A.inv_r;
+        A.co[nd] = cz + dcv;
+        r += dcv * (A.rd * dcv + g + g);
+        if (was) {
+          const double gw = (double)(float)(gi + dw);
+          const double dcw = ((xi - gw) - gw) * A.inv_r;
+          r -= dcw * (A.rd * dcw + gw + gw);
+        }
+      }
+      nrm += r;
+    }
+    // hints of the emitted edges: interior, then the bend's touch
+    for (int e = s0; e < bk && e < m - 1; ++e) {
+      const int side = e == bk - 1 ? bt : 0;
+      uint16_t* wp = A.sg + (e / TP) * C32 + c32;
+      const int q = e % TP;
+      unsigned w = *wp & ~((1u << q) | (1u << (8 + q)));
+      w |= side > 0 ? (1u << q) : (side < 0 ? (1u << (8 + q)) : 0u);
+      *wp = (uint16_t)w;
+    }
+    s0 = bk;
+    if (stop) break;
+  }
+  return nrm;
+}
+
+template <int ROLE, bool ROWLIKE, bool VER = false>
 __global__ void __launch_bounds__(WARPS * 32)
     k_sweep(const __grid_constant__ Args A, const __grid_constant__ Maps M) {
   extern __shared__ __align__(128) unsigned char smem_raw[];  // TMA boxes land 128-B aligned
+  // device-side choice between the two sweeps of a family (both are launched;
+  // the one the mode word does not select returns at once)
+  if (A.vmode != nullptr && ((*A.vmode == 1) != VER)) return;
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const Fam F = A.F;
@@ -326,6 +550,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int rhi = __reduce_max_sync(0xffffffffu, has ? stop : 0);
   const int t_first = rlo == 0x7fffffff ? 0 : rlo / TP;
   const int ntiles = (rhi + TP - 1) / TP;
+  const int ntile_sg = (m + TP - 1) / TP;  // hint words per chain
 
   // ---- lane state: stackless taut string in the anchor frame.  The scan runs
   // in R = fp32 for the in-place roles (values are taken relative to the
@@ -347,6 +572,21 @@ __global__ void __launch_bounds__(WARPS * 32)
   R fs = -RINF, Lf = -RINF;  // max slope to the floor points; fs * (k - i0)
   unsigned smask = 0u;        // segment starts inside the ring (bit = slot)
   double zs = 0.0, qs = 0.0;  // retire carry: z at the current segment start, q there
+  // Segment hints (SCAN writes them for the next iteration's VER sweep): the
+  // side of edge e is the sign of the jump between the segment values around
+  // it, found at retire time from consecutive segment starts.  Bit 7 + q of
+  // hup / hdn is edge k0 + q - 1 of the tile being retired (its first bit is
+  // the previous tile's last edge, so a tile's word is stored one retire later).
+#ifdef PCB_NO_HINT_WRITE  // experiment: scans without hint writes
+  const bool SGW = false;
+#else
+  // (hints are written only by the scan right before a verified probe: mode 2)
+  const bool SGW = !VER && ROLE != SHADOW && A.sg != nullptr && A.vmode && *A.vmode == 2;
+#endif
+  double xprev = __longlong_as_double(0x7ff8000000000000ll);  // NaN: no previous segment
+  unsigned hup = 0u, hdn = 0u;
+  unsigned hold_prev = 0u, hold_cur = 0u;  // hint words before this iteration (change count)
+  bool hchanged = false;
 
   // retire-only inputs prefetched into registers (G for MID/LAST, X for LAST)
   float gpre[TP], xpre[TP];
@@ -377,19 +617,24 @@ __global__ void __launch_bounds__(WARPS * 32)
   const R eoff = (has && stop < m && etouch != 0)
                      ? (R)((double)etouch * (double)A.wf[((stop - 1) * C32 + c32)]) : R(0);
 
+  unsigned long long sw = 0ull;  // VER: hint words of the issued tiles (16 bits per slot T & 3)
   auto issue = [&](int T) {
     const int k0 = T * TP;
     PCB_CNT(3, 1);
+    if (VER && valid && T < ntile_sg) {
+      const unsigned sh = (unsigned)(T & (NT - 1)) * 16u;
+      sw = (sw & ~(0xffffull << sh)) | ((unsigned long long)A.sg[T * C32 + c32] << sh);
+    }
     if (ROLE == MID || ROLE == LAST) {
       // pull the tile's retire-only inputs (G, X: natural layout) towards L2
       // now, so the register prefetch a round before retirement hits L2
       if (!ROWLIKE) {  // 32 chains = 32 consecutive nodes per position: lanes 0-7 G, 8-15 X
         const int q = lane & 7, pos = k0 + q;
         if (warp_live && pos < m && (lane < 8 || (ROLE == LAST && lane < 16)))
-          l2_prefetch((lane < 8 ? (const void*)(A.G + node(b0, pos))
+          l2_prefetch((lane < 8 ? (const void*)(A.Gi + node(b0, pos))
                                 : (const void*)(A.X + node(b0, pos))));
       } else if (valid && k0 < m) {  // each lane: its chain's 8 positions
-        l2_prefetch(A.G + node(base32, k0));
+        l2_prefetch(A.Gi + node(base32, k0));
         if (ROLE == LAST) l2_prefetch(A.X + node(base32, k0));
       }
     }
@@ -446,7 +691,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int pos = k0 + q;
         const bool pr = valid && pos < m;
         const int nd = pr ? node(base32, pos) : 0;
-        gpre[q] = pr ? A.G[nd] : 0.f;
+        gpre[q] = pr ? A.Gi[nd] : 0.f;
         if (ROLE == LAST) xpre[q] = pr ? A.X[nd] : 0.f;
       }
     } else {
@@ -457,7 +702,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int bi = bB[ib];
         const bool pr = i < nvalid && pos < m;
         const int nd = pr ? node(bi, pos) : 0;
-        gpre[ib] = pr ? A.G[nd] : 0.f;
+        gpre[ib] = pr ? A.Gi[nd] : 0.f;
         if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : 0.f;
       }
     }
@@ -494,6 +739,15 @@ __global__ void __launch_bounds__(WARPS * 32)
           // (SHADOW: the fp64 q split over the dead p / weight slots)
           qs = (ROLE == SHADOW) ? __hiloint2double(__float_as_int(ra[ix]), __float_as_int(rp[ix]))
                                 : (double)ra[ix];
+          if (SGW) {
+            // the segment's prox value; jumps below 1e-6 (fp32 rounding of q)
+            // count as none, so the change count sees segmentation changes
+            // rather than rounding noise
+            const double xs = zj - qs, dj = xs - xprev;
+            hup |= (unsigned)(dj > 1e-6) << (7 + q);
+            hdn |= (unsigned)(dj < -1e-6) << (7 + q);
+            xprev = xs;
+          }
         }
         const double pn = (zj - zs) + qs;
         if (ROLE == SHADOW) {
@@ -504,7 +758,7 @@ __global__ void __launch_bounds__(WARPS * 32)
           const float p32 = (float)pn;
           const double d = (double)p32 - (double)pold;
           nq = nrm_d(d, nq);
-          A.p[(pos * C32 + c32)] = p32;
+          A.po[(pos * C32 + c32)] = p32;
           if (!ROWLIKE) {
             const int nd = node(base32, pos);
             if (ROLE == FIRST) {
@@ -515,9 +769,9 @@ __global__ void __launch_bounds__(WARPS * 32)
               const float g32 = (float)((double)gpre[q] + d);
               const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
-              A.X[nd] = (float)xn;
+              A.Xo[nd] = (float)xn;
               const double dcv = (xn - g) * A.inv_r;
-              A.c[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
+              A.co[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
               if (A.export_g) A.G[nd] = g32;
               nq = nrm_last(dcv, g, A.rd, nq);
             }
@@ -528,6 +782,19 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
     }
     smask &= ~(0xffu << ((k0 & (RL - 1))));
+    if (SGW && valid) {
+      // the word of tile T - 1 is complete now (its last edge's side came from
+      // a segment start at k0); the old word of tile T is read for the next one
+      hold_prev = hold_cur;
+      if (T < ntile_sg) hold_cur = A.sg[T * C32 + c32];
+      if (T > t_first) {
+        const unsigned wd = (hup & 0xffu) | ((hdn & 0xffu) << 8);
+        hchanged |= wd != hold_prev;
+        A.sg[(T - 1) * C32 + c32] = (uint16_t)wd;
+      }
+      hup >>= 8;
+      hdn >>= 8;
+    }
     if (ROWLIKE) {
       __syncwarp();
       const int q = lane & 7;
@@ -550,9 +817,9 @@ __global__ void __launch_bounds__(WARPS * 32)
             const float g32 = (float)((double)gpre[ib] + (double)ra[ix]);
             const double g = (double)g32;
             const double xn = (double)xpre[ib] - g;
-            A.X[nd] = (float)xn;
+            A.Xo[nd] = (float)xn;
             const double dcv = (xn - g) * A.inv_r;
-            A.c[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
+            A.co[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
             if (A.export_g) A.G[nd] = g32;
             double& nq = (ib & 1) ? nb : na;
             nq = nrm_last(dcv, g, A.rd, nq);
@@ -710,7 +977,101 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
   };
 
-  if (warp_live && rhi > 0) {
+  // ---------------- VER: verify last iteration's segmentation as a candidate.
+  // Lanes advance in lockstep, one position per step.  Each candidate segment
+  // [i0, k] (ended by a hinted tube touch, a zero weight or the chain end) gets
+  // its value from the sum of z and the duals at its ends (u = -a at a ceiling
+  // touch, +a at a floor touch, 0 at a piece end), and the complete KKT
+  // conditions are checked: |u_j| <= a_j on the interior edges (a cone of
+  // slopes, as in the taut string) and the sign of the jump at a touch.  A
+  // segment that fails is still emitted; its lane is repaired after the sweep
+  // (repair_lane: a taut string between true points around the failures).
+  int ff = 0x7fffffff, fl = -1;  // VER: first failing segment start, last failing position
+  if (VER && warp_live && rhi > 0) {
+    constexpr float FINF = __builtin_huge_valf();
+    bool vdone = !has;            // closed the chain's last segment, or abandoned
+    double vt = 0.0, tp = 0.0;    // anchor (z at i0) of the open / previous segment
+    float Q = 0.f, LO = -FINF, HI = FINF, xrp = 0.f;
+    int sideL = 0;                // side of the open segment's left edge (0: piece start)
+    auto vtrip = [&](int k0, int q, unsigned w) {
+      const int kk = k0 + q;
+      if (vdone || kk >= stop) return;
+      const int ix = tix(k0, q);
+      const double z = rz[ix];
+      const float a = ra[ix];
+      const bool last = kk == m - 1;
+      const float ak = last ? 0.f : a;
+      const int side = (int)((w >> q) & 1u) - (int)((w >> (8 + q)) & 1u);
+      const bool fresh = kk == i0;
+      vt = fresh ? z : vt;
+      const float zr = (float)(z - vt);
+      Q += zr;
+      const float inv = rcp_r<float>(kk - i0 + 1);
+      const bool piece = last || ak == 0.f;
+      const bool cl = piece || side != 0;
+      const float uR = piece ? 0.f : (side > 0 ? -ak : ak);
+      if (cl) {
+        const float xr = (Q - uR) * inv;                  // segment value - vt
+        const float dx = (xr - xrp) + (float)(vt - tp);   // jump over the left edge
+        const float tol = 4e-6f * (1.f + fabsf(xr));
+        const bool bad = (LO > xr + tol) || (xr > HI + tol) || ((float)sideL * dx < -tol);
+        ff = bad ? min(ff, i0) : ff;
+        fl = bad ? kk : fl;
+        ra[rx(lane, i0)] = -xr;  // q = p'(i0) = z(i0) - x; the retire rebuilds the rest
+        smask |= 1u << (i0 & (RL - 1));
+        xrp = xr;
+        tp = vt;
+        sideL = piece ? 0 : side;
+        Q = uR;
+        LO = -FINF;
+        HI = FINF;
+        i0 = kk + 1;
+        vdone = i0 >= stop;
+      } else {  // interior edge kk: (Q - a) / len <= x - vt <= (Q + a) / len
+        LO = fmaxf(LO, (Q - ak) * inv);
+        HI = fminf(HI, (Q + ak) * inv);
+      }
+    };
+    int T = t_first;  // next tile to verify
+    while (t_ld < ntiles && t_ld - t_first < NT) issue(t_ld++);
+    for (;;) {
+      if (T < t_ld) {
+        land(T);
+        to_z(T);
+        t_rdy = T + 1;
+        const unsigned w = (unsigned)(sw >> ((unsigned)(T & (NT - 1)) * 16u)) & 0xffffu;
+#pragma unroll
+        for (int q = 0; q < TP; ++q) vtrip(T * TP, q, w);
+        ++T;
+      }
+      if (__all_sync(0xffffffffu, vdone)) {
+        for (int X = T; X < t_ld; ++X) land(X);  // nothing may be in flight at exit
+        if (!use_tma) {
+          cp_wait(0);
+          __syncwarp();
+        }
+        for (int X = t_lo; X < t_ld; ++X) retire(X);
+        break;
+      }
+      const int front = __reduce_min_sync(0xffffffffu, vdone ? 0x7fffffff : i0);
+      while (t_lo < T && (t_lo + 1) * TP <= front) retire(t_lo++);
+      if (t_lo < T && pre_tile != t_lo) prefetch(t_lo);  // G / X of the next tile to retire
+      if (t_ld - t_lo == NT && T == t_ld) {
+        // ring full and a lane's open segment spans it: that lane gives up
+        // here (its positions from i0 on stay unemitted) and is repaired
+        if (!vdone && i0 < (t_lo + 1) * TP) {
+          ff = min(ff, i0);
+          fl = m;
+          vdone = true;
+        }
+        __syncwarp();
+        retire(t_lo++);
+      }
+      __syncwarp();
+      while (t_ld < ntiles && t_ld - t_lo < NT) issue(t_ld++);
+    }
+  }
+  if (!VER && warp_live && rhi > 0) {
     while (t_ld < ntiles && t_ld - t_first < NT) issue(t_ld++);
     land(t_first);
     to_z(t_first);
@@ -737,6 +1098,11 @@ __global__ void __launch_bounds__(WARPS * 32)
           __syncwarp();
         }
         for (int T = t_lo; T < t_ld; ++T) retire(T);
+        if (SGW && valid && ntiles > t_first) {  // the last tile's word
+          const unsigned wd = (hup & 0xffu) | ((hdn & 0xffu) << 8);
+          hchanged |= wd != hold_cur;
+          A.sg[(ntiles - 1) * C32 + c32] = (uint16_t)wd;
+        }
         break;
       }
       // ---------------- retire tiles every lane has emitted
@@ -754,16 +1120,22 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
     }
   }
-  if (ROLE != SHADOW) {
-    __shared__ double sh[WARPS];
+  if (VER) {
+    __syncwarp();  // the sweep's writes (mode-B lanes write other chains) are visible
+    const bool dirty = valid && ff != 0x7fffffff;
+#ifndef PCB_NO_REPAIR  // timing experiments only: results are wrong without the repair
+    if (dirty) nrm += repair_lane<ROLE, ROWLIKE>(A, c32, base32, ff, fl, i0);
+#endif
+    const int nch = __popc(__ballot_sync(0xffffffffu, dirty));
+    if (lane == 0 && nch && A.vcount) atomicAdd(A.vcount, nch);
+  }
+  if (SGW && warp_live) {  // chains whose hints changed: the mode policy's signal
+    const int nch = __popc(__ballot_sync(0xffffffffu, hchanged && valid));
+    if (lane == 0 && nch && A.vcount) atomicAdd(A.vcount, nch);
+  }
+  if (ROLE != SHADOW) {  // step-norm partial: one slot per warp (no block barrier)
     const double v = warp_sum(nrm);
-    if (lane == 0) sh[wib] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < WARPS; ++w) t += sh[w];
-      A.parts[blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = t;
-    }
+    if (lane == 0) A.parts[(blockIdx.x + (int64_t)blockIdx.y * gridDim.x) * WARPS + wib] = v;
   }
 }
 
@@ -777,81 +1149,6 @@ __global__ void __launch_bounds__(WARPS * 32)
 // thread scans both speculative strings (fp64 stackless scan, data from
 // global memory) bend by bend until they share a bend point, or gives up
 // after `window` positions (merge = -1: the previous unit continues).
-struct Spec {
-  int i0, pe, k, c0x, f0x;
-  double t, skr, cs, fs, Lc, Lf;
-  bool fresh;
-};
-
-template <class ZA>
-__device__ __forceinline__ void spec_next_bend(Spec& S, int m, const ZA& za, int* bk_out,
-                                               int* bt_out) {
-  for (;;) {
-    const int kp = S.k;
-    double zabs, av;
-    za(kp, &zabs, &av);
-    S.k = kp + 1;
-    if (S.fresh) {
-      S.t = zabs;
-      S.fresh = false;
-    }
-    S.skr += zabs - S.t;
-    const bool inner = S.k < m;
-    const double rk = inner ? av : 0.0;
-    if (inner && av == 0.0) S.pe = S.k;
-    const double inv = rcp_r<double>(S.k - S.i0);
-    S.Lc += S.cs;
-    S.Lf += S.fs;
-    const double u = S.skr + rk;
-    if (S.c0x < 0 || u <= S.Lc) {
-      S.c0x = S.k;
-      S.cs = u * inv;
-      S.Lc = u;
-    }
-    int bk = -1, bt = 0;
-    double fill = 0.0;
-    if (S.f0x >= 0 && S.cs < S.fs) {
-      bk = S.f0x; bt = -1; fill = S.fs;
-    } else {
-      const double l = S.skr - rk;
-      if (S.f0x < 0 || l >= S.Lf) {
-        S.f0x = S.k;
-        S.fs = l * inv;
-        S.Lf = l;
-      }
-      if (S.fs > S.cs) {
-        bk = S.c0x; bt = 1; fill = S.cs;
-      } else if (S.k == S.pe) {
-        if (S.c0x != S.pe && S.Lc < S.skr) {
-          bk = S.c0x; bt = 1; fill = S.cs;
-        } else if (S.f0x != S.pe && S.Lf > S.skr) {
-          bk = S.f0x; bt = -1; fill = S.fs;
-        } else {
-          bk = S.pe; bt = 0; fill = S.skr * inv;
-        }
-      }
-    }
-    if (bk >= 0) {
-      (void)fill;
-      double ab = 0.0;
-      if (bt != 0) {
-        double dz;
-        za(bk - 1, &dz, &ab);
-      }
-      const bool piece_end = bk == S.pe;
-      S.i0 = S.k = bk;
-      S.fresh = true;
-      S.skr = piece_end ? 0.0 : -(double)bt * ab;
-      if (piece_end) S.pe = m;
-      S.c0x = S.f0x = -1;
-      S.cs = S.fs = S.Lc = S.Lf = 0.0;
-      *bk_out = bk;
-      *bt_out = piece_end ? 0 : bt;
-      return;
-    }
-  }
-}
-
 // One warp = 32 chains at block b.  The first MW positions from the block
 // gate are staged in shared memory with coalesced cp.async (mode A / mode B
 // like the sweep); merges almost always happen inside that window, positions

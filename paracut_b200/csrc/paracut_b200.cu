@@ -384,6 +384,7 @@ __global__ void __launch_bounds__(FAM_BLOCK) k_tv1d(const double* s, const doubl
 }  // namespace
 
 #include "fast_sweep.cuh"
+#include "lean_verify.cuh"
 #include "exact_sweep.cuh"
 
 namespace {
@@ -1096,6 +1097,17 @@ struct pcb_solver {
   int nbk[MAXR]{};        // fp32 path: blocks per chain (intra-chain split), 1 = whole chains
   int lbk[MAXR]{};        // block length (positions)
   DBuf<int> merge;        // merge points, family j at merge_off[j] (nbk[j] * C_j entries)
+  // Double-buffered fp32 step with verified sweeps:
+  // alternate state buffers (the step reads p32 / cdrift / X32 and writes
+  // these, then the two sets swap), per-family segment hints and the
+  // per-family device mode words {mode (1 = VER), count}.
+  bool dbuf = false;
+  int vtheta = 10;  // verify when fewer than vtheta % of a family's chains changed
+  DBuf<float> p32b, G32b, X32b;
+  DBuf<double> cdriftb;
+  DBuf<uint16_t> sg[MAXR];
+  DBuf<int> vstate;
+  pcb::fast::Maps maps2[MAXR]{};  // TMA descriptors of the alternate buffers
   int64_t merge_off[MAXR]{};
   // merges of a step run on a side stream, overlapping the sweeps (they
   // depend only on the state at the start of the step)
@@ -1117,7 +1129,9 @@ struct pcb_solver {
   }
   pcb_solver() {
     bind(w, z, y, p32, cdrift, X32, G32, tmp, yprev, bits, xcur, bestlab, bestx, parts, vals,
-         norms, sp_cx, sp_fx, sp_cy, sp_fy, packed, normlog, lablog, merge);
+         norms, sp_cx, sp_fx, sp_cy, sp_fy, packed, normlog, lablog, merge, p32b, G32b, X32b,
+         cdriftb, vstate);
+    bind_arr(sg);
     bind_arr(dirw);
     bind_arr(dirw_base);
     bind_arr(wf64);
@@ -1461,8 +1475,10 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
-template <int ROLE, bool ROWLIKE>
-int launch_sweep(pcb_solver* h, const pcb::fast::Args& a, const pcb::fast::Maps& M) {
+template <int ROLE, bool ROWLIKE, bool VER = false>
+int launch_sweep(pcb_solver* h, const pcb::fast::Args& a_in, const pcb::fast::Maps& M) {
+  pcb::fast::Args a = a_in;
+  pcb::fast::args_inplace(a);
 #ifndef PCB_RING_PAD
 #define PCB_RING_PAD 0  // experiment knob: extra dynamic smem per block (occupancy probes)
 #endif
@@ -1471,13 +1487,13 @@ int launch_sweep(pcb_solver* h, const pcb::fast::Args& a, const pcb::fast::Maps&
   static unsigned set_mask = 0;
   const unsigned bit = 1u << (h->device & 31);
   if (!(set_mask & bit)) {
-    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE>,
+    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     set_mask |= bit;
   }
   const int per = pcb::fast::WARPS * 32;
   const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
-  pcb::fast::k_sweep<ROLE, ROWLIKE><<<g, per, bytes, h->stream>>>(a, M);
+  pcb::fast::k_sweep<ROLE, ROWLIKE, VER><<<g, per, bytes, h->stream>>>(a, M);
   LAUNCH_CHECK(h);
   return 0;
 }
@@ -1486,6 +1502,41 @@ template <int ROLE>
 int launch_role(pcb_solver* h, const pcb::fast::Args& a, int j) {
   return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a, h->maps[j])
                                : launch_sweep<ROLE, false>(h, a, h->maps[j]);
+}
+
+// SCAN and VER sweeps of one family in the double-buffered step: both are
+// launched, the device mode word picks the one that runs
+template <int ROLE, bool ROWLIKE>
+int launch_verify(pcb_solver* h, const pcb::fast::Args& a_in) {
+  pcb::fast::Args a = a_in;
+  pcb::fast::args_inplace(a);
+  constexpr int per = pcb::fast::LV_WARPS * 32;
+  const unsigned g = (unsigned)((a.F.C + per - 1) / per);
+  pcb::fast::k_verify<ROLE, ROWLIKE><<<g, per, 0, h->stream>>>(a);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+// PCB_VERIFY_RING=1: the verified sweep inside the ring kernel (A/B experiments)
+bool verify_ring() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PCB_VERIFY_RING");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int ROLE>
+int launch_role_v(pcb_solver* h, const pcb::fast::Args& a, int j) {
+  const bool rl = fam_rowlike(a.F.kind);
+  if (int e = rl ? launch_sweep<ROLE, true>(h, a, h->maps[j]) : launch_sweep<ROLE, false>(h, a, h->maps[j]))
+    return e;
+  if (!a.vmode) return 0;
+  if (verify_ring())
+    return rl ? launch_sweep<ROLE, true, true>(h, a, h->maps[j])
+              : launch_sweep<ROLE, false, true>(h, a, h->maps[j]);
+  return rl ? launch_verify<ROLE, true>(h, a) : launch_verify<ROLE, false>(h, a);
 }
 
 // merge points of family j for the current state (before its sweep), on
@@ -1547,8 +1598,8 @@ EncodeTiledFn encode_tiled() {
 // TMA maps for the strided families whose warps cover 32 consecutive nodes
 // (cols; 3D y with D2 % 32 == 0; 3D z).  Others keep the per-lane cp.async.
 // PCB_TMA=0 disables them.
-void build_maps(pcb_solver* h) {
-  for (int j = 0; j < MAXR; ++j) h->maps[j] = pcb::fast::Maps{};
+void build_maps_for(pcb_solver* h, float* pbuf, double* cbuf, pcb::fast::Maps* maps) {
+  for (int j = 0; j < MAXR; ++j) maps[j] = pcb::fast::Maps{};
   const char* env = getenv("PCB_TMA");
   if (env && env[0] == '0') return;
   EncodeTiledFn fn = encode_tiled();
@@ -1569,7 +1620,7 @@ void build_maps(pcb_solver* h) {
     const cuuint64_t dp[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
     const cuuint64_t da[2] = {(cuuint64_t)F.C, (cuuint64_t)(F.m - 1)};
     const cuuint64_t sp[1] = {(cuuint64_t)F.C * 4};
-    CUresult r1 = fn(&M.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(h->p32.p + (int64_t)j * h->n), dp, sp, box2, es2,
+    CUresult r1 = fn(&M.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(pbuf + (int64_t)j * h->n), dp, sp, box2, es2,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     CUresult r2 = fn(&M.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)h->wf32[j].p, da, sp, box2,
@@ -1579,27 +1630,89 @@ void build_maps(pcb_solver* h) {
     if (!c3) {
       const cuuint64_t dc[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
       const cuuint64_t sc[1] = {(cuuint64_t)F.ns * 8};
-      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)h->cdrift.p, dc, sc, box2, es2,
+      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)cbuf, dc, sc, box2, es2,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       const cuuint64_t dc[3] = {(cuuint64_t)F.cdiv, (cuuint64_t)F.m, (cuuint64_t)(F.C / F.cdiv)};
       const cuuint64_t sc[2] = {(cuuint64_t)F.ns * 8, (cuuint64_t)F.chi * 8};
       const cuuint32_t box3[3] = {32, (cuuint32_t)TP, 1}, es3[3] = {1, 1, 1};
-      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)h->cdrift.p, dc, sc, box3, es3,
+      r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)cbuf, dc, sc, box3, es3,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) continue;
     M.tma = 1;
     M.c3 = c3 ? 1 : 0;
-    h->maps[j] = M;
+    maps[j] = M;
   }
 }
 
+void build_maps(pcb_solver* h) {
+  build_maps_for(h, h->p32.p, h->cdrift.p, h->maps);
+  if (h->dbuf) build_maps_for(h, h->p32b.p, h->cdriftb.p, h->maps2);
+}
+
+// step-norm partial slots of a family sweep: one per warp (and unit)
 int fam_units(const pcb_solver* h, int j) {
   const int per = pcb::fast::WARPS * 32;
-  return (int)((h->fam[j].C + per - 1) / per) * (h->nbk[j] > 1 ? h->nbk[j] : 1);
+  return (int)((h->fam[j].C + per - 1) / per) * pcb::fast::WARPS * (h->nbk[j] > 1 ? h->nbk[j] : 1);
+}
+
+// Per family {mode, count, cool, backoff}, then {verified sweeps, repaired
+// chains, scan sweeps, changed chains} (int64) per family.
+constexpr int VS_FAM = 4;
+constexpr int VSTATE_INTS = VS_FAM * MAXR + 8 * MAXR;
+constexpr int VS_COOL0 = 12;  // plain iterations before the first verified probe
+
+// Mode policy of the verified sweeps, once per double-buffered step (device
+// side, so graph-capturable and deterministic: it depends only on integer
+// counts).  Modes: 0 scan, 2 scan that writes segment hints (the iteration
+// before a probe), 1 verify.  A family verifies while fewer than theta % of
+// its chains needed a repair; otherwise it scans for `backoff` iterations
+// (doubling, up to 256) before the next probe.
+struct VModeArgs {
+  int r;
+  int64_t C[MAXR];  // 0: family without hints (always scans)
+  int theta_pct;
+};
+
+__global__ void k_vmode(int* vs, VModeArgs va) {
+  const int j = threadIdx.x;
+  if (j >= va.r || va.C[j] == 0) return;
+  int* f = vs + VS_FAM * j;
+  const int64_t cnt = f[1];
+  long long* st = reinterpret_cast<long long*>(vs + VS_FAM * MAXR) + 4 * j;
+  const int mode = f[0];
+  st[mode == 1 ? 0 : 2] += 1;
+  st[mode == 1 ? 1 : 3] += cnt;
+  if (mode == 1) {
+    if (cnt * 100 >= va.C[j] * (int64_t)va.theta_pct) {
+      f[3] = min(2 * f[3], 256);
+      f[2] = f[3];
+      f[0] = 0;
+    }
+  } else if (mode == 2) {
+    f[0] = 1;
+  } else if (--f[2] <= 0) {
+    f[0] = 2;
+  }
+  f[1] = 0;
+}
+
+template <class T>
+void swap_buf(DBuf<T>& a, DBuf<T>& b) {
+  std::swap(a.p, b.p);
+  std::swap(a.n, b.n);
+  std::swap(a.pooled, b.pooled);
+}
+
+// after a double-buffered step the alternate buffers hold the state
+void swap_state(pcb_solver* h) {
+  swap_buf(h->p32, h->p32b);
+  swap_buf(h->cdrift, h->cdriftb);
+  swap_buf(h->X32, h->X32b);
+  for (int j = 0; j < MAXR; ++j) std::swap(h->maps[j], h->maps2[j]);
 }
 
 // one fused fp32 iteration over the handle's active families; partials of
@@ -1640,6 +1753,13 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
       }
     }
   }
+  // double-buffered step (plain single-handle iterations): read the current
+  // state, write the alternate buffers, swap at the end; families with segment
+  // hints launch both the SCAN and the verified sweep (device mode word)
+  const unsigned all = (1u << h->r) - 1u;
+  const bool dbuf = h->dbuf && flags == 0 && (h->fmask & all) == all && na == h->r && na >= 2;
+  float* Gb[2] = {h->G32.p, h->G32b.p};
+  int gcur = 0;  // Gb[gcur]: the accumulator the previous role wrote
   int64_t off = 0;
   for (int q = 0; q < na; ++q) {
     const int j = act[q];
@@ -1651,6 +1771,33 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
                       h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
                       (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
+    if (dbuf) {
+      a.po = h->p32b.p + (int64_t)j * h->n;
+      a.co = h->cdriftb.p;
+      a.Xo = h->X32b.p;
+      if (role == pcb::fast::FIRST) {  // G = d
+        a.G = Gb[0];
+        a.Gi = Gb[0];
+        gcur = 0;
+      } else if (role == pcb::fast::MID && (F.kind == K_ZZ0 || F.kind == K_ZZ1)) {
+        // a zig-zag family leaves border nodes out: its G += d stays in place
+        // (those nodes keep G), and it gets no hints (no verified sweep)
+        a.G = Gb[gcur];
+        a.Gi = Gb[gcur];
+      } else if (role == pcb::fast::MID) {  // G' = G + d into the other buffer
+        a.Gi = Gb[gcur];
+        a.G = Gb[gcur ^ 1];
+        gcur ^= 1;
+      } else {  // LAST reads the final accumulator
+        a.G = Gb[gcur];
+        a.Gi = Gb[gcur];
+      }
+      if (h->sg[j].p) {
+        a.sg = h->sg[j].p;
+        a.vmode = h->vstate.p + VS_FAM * j;
+        a.vcount = h->vstate.p + VS_FAM * j + 1;
+      }
+    }
     int rc = 0;
     if (side_merge[j]) {
       CUDA_TRY(cudaStreamWaitEvent(h->stream, h->ev_merge[j], 0));
@@ -1660,13 +1807,22 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     prof_begin(h, j);
     if (!side_merge[j]) rc = launch_merge(h, j, a);
     if (!rc) {
-      if (role == pcb::fast::FIRST) rc = launch_role<pcb::fast::FIRST>(h, a, j);
-      else if (role == pcb::fast::MID) rc = launch_role<pcb::fast::MID>(h, a, j);
-      else rc = launch_role<pcb::fast::LAST>(h, a, j);
+      if (role == pcb::fast::FIRST) rc = launch_role_v<pcb::fast::FIRST>(h, a, j);
+      else if (role == pcb::fast::MID) rc = launch_role_v<pcb::fast::MID>(h, a, j);
+      else rc = launch_role_v<pcb::fast::LAST>(h, a, j);
     }
     prof_end(h);
     if (rc) return rc;
     off += fam_units(h, j);
+  }
+  if (dbuf) {
+    VModeArgs va{};
+    va.r = h->r;
+    for (int j = 0; j < h->r; ++j) va.C[j] = h->sg[j].p ? h->fam[j].C : 0;
+    va.theta_pct = h->vtheta;
+    k_vmode<<<1, 32, 0, h->stream>>>(h->vstate.p, va);
+    LAUNCH_CHECK(h);
+    swap_state(h);
   }
   k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, off, norm_slot,
                                             (flags & PCB_STEP_NORM_RAW) ? 0 : 1);
@@ -1733,6 +1889,50 @@ int choose_split(pcb_solver* h) {
     if (int e = h->merge.alloc(need)) return e;
   const char* ov = getenv("PCB_OVERLAP_MERGE");
   h->overlap_merges = !(ov && ov[0] == '0');
+  return 0;
+}
+
+// Double buffers, segment hints and mode words of the verified sweeps
+// (PCB_VERIFY=0 keeps the single-buffer SCAN step).  Hints only for families
+// swept as whole chains (a split family keeps its merge-point units).
+int reset_verify(pcb_solver* h);
+
+int setup_verify(pcb_solver* h) {
+  const char* env = getenv("PCB_VERIFY");
+  h->dbuf = !(env && env[0] == '0') && h->r >= 2;
+  if (!h->dbuf) return 0;
+  const char* th = getenv("PCB_VERIFY_THETA");  // tuning / test knob (percent of chains)
+  h->vtheta = th ? atoi(th) : 10;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (int e = h->p32b.alloc(rn)) return e;
+  if (int e = h->cdriftb.alloc(h->n)) return e;
+  if (int e = h->X32b.alloc(h->n)) return e;
+  if (int e = h->G32b.alloc(h->n)) return e;
+  CUDA_TRY(cudaMemset(h->p32b.p, 0, rn * sizeof(float)));
+  for (int j = 0; j < h->r; ++j) {
+    const Fam& F = h->fam[j];
+    // row-like families only: their scan stages c through per-lane cp.async
+    // rows, where the verified sweep's contiguous vector loads win; the
+    // strided families' TMA-fed scan is as fast as a verified sweep
+    if (F.C == 0 || F.m < 2 || h->nbk[j] > 1 || !fam_rowlike(F.kind) || F.kind == K_ZZ0 ||
+        F.kind == K_ZZ1 || F.m >= (1 << 16))
+      continue;
+    const int64_t cnt = (int64_t)((F.m + pcb::fast::TP - 1) / pcb::fast::TP) * F.C;
+    if (int e = h->sg[j].alloc(cnt)) return e;
+    CUDA_TRY(cudaMemset(h->sg[j].p, 0, cnt * sizeof(uint16_t)));
+  }
+  if (int e = h->vstate.alloc(VSTATE_INTS)) return e;
+  CUDA_TRY(cudaMemset(h->vstate.p, 0, VSTATE_INTS * sizeof(int)));
+  return reset_verify(h);
+}
+
+// scan first after a new state (the hints describe the old one)
+int reset_verify(pcb_solver* h) {
+  if (!h->vstate.p) return 0;
+  static const int init[VS_FAM * MAXR] = {0, 0, VS_COOL0, VS_COOL0, 0, 0, VS_COOL0, VS_COOL0,
+                                          0, 0, VS_COOL0, VS_COOL0, 0, 0, VS_COOL0, VS_COOL0};
+  CUDA_TRY(cudaMemcpyAsync(h->vstate.p, init, sizeof(init), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(cudaStreamSynchronize(h->stream));  // (init is pageable host memory)
   return 0;
 }
 
@@ -1931,10 +2131,11 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
     if ((rc = h->G32.alloc(n))) return bail(rc);
     phase("alloc");
     if ((rc = ensure_wf32(h))) return bail(rc);
-    build_maps(h);
-    phase("family weights");
     if ((rc = choose_split(h))) return bail(rc);
     phase("split");
+    if ((rc = setup_verify(h))) return bail(rc);
+    build_maps(h);
+    phase("family weights");
   }
   if (precision == PCB_F64)  // hull spill for the exact kernels (f32 path: lazily, project_K only)
     if ((rc = ensure_spill(h))) return bail(rc);
@@ -2031,8 +2232,14 @@ int pcb_debug_counters(uint64_t* out, int reset) {
     CUDA_TRY(cudaMemcpyToSymbol(pcb::fast::g_count, z, sizeof(z)));
   }
 #else
-  (void)reset;
-  for (int i = 0; i < 8; ++i) out[i] = 0;
+  unsigned long long v[8];
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpyFromSymbol(v, pcb::fast::g_rep, sizeof(v)));
+  for (int i = 0; i < 8; ++i) out[i] = v[i];
+  if (reset) {
+    unsigned long long z[8] = {};
+    CUDA_TRY(cudaMemcpyToSymbol(pcb::fast::g_rep, z, sizeof(z)));
+  }
 #endif
   return 0;
 }
@@ -2139,6 +2346,7 @@ int pcb_init_cold(pcb_solver* h) {
     k_init_exact<<<g, 256, 0, h->stream>>>(h->z.p, h->w.p, h->n, h->r);
   } else {
     k_init_fast<<<g, 256, 0, h->stream>>>(h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, h->r);
+    if (int e = reset_verify(h)) return e;
   }
   LAUNCH_CHECK(h);
   h->have_state = true;
@@ -2159,6 +2367,7 @@ int pcb_set_z(pcb_solver* h, const double* z) {
     k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
         h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, famset(h), h->D);
     LAUNCH_CHECK(h);
+    if (int e = reset_verify(h)) return e;
   }
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->have_state = true;
@@ -2684,6 +2893,27 @@ int pcb_device_buffer(pcb_solver* h, int which, uintptr_t* ptr, int64_t* count) 
     default: return fail(PCB_E_ARG, "unknown buffer id %d", which);
   }
   if (!*ptr) return fail(PCB_E_STATE, "buffer %d not allocated for this precision", which);
+  return 0;
+}
+
+int pcb_verify_stats(pcb_solver* h, int* modes, int64_t* sweeps, int64_t* repaired,
+                     int64_t* scans, int64_t* changed) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (int e = set_dev(h)) return e;
+  int v[VSTATE_INTS] = {};
+  if (h->vstate.p) {
+    CUDA_TRY(cudaMemcpyAsync(v, h->vstate.p, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(cudaStreamSynchronize(h->stream));
+  }
+  long long st[4 * MAXR];
+  memcpy(st, v + VS_FAM * MAXR, sizeof(st));
+  for (int j = 0; j < h->r; ++j) {
+    if (modes) modes[j] = h->sg[j].p ? v[VS_FAM * j] : -1;
+    if (sweeps) sweeps[j] = st[4 * j];
+    if (repaired) repaired[j] = st[4 * j + 1];
+    if (scans) scans[j] = st[4 * j + 2];
+    if (changed) changed[j] = st[4 * j + 3];
+  }
   return 0;
 }
 
