@@ -143,6 +143,21 @@ int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
  * and pcb_apply_g leaves their norm term out.  n_own = n: no halo. */
 int pcb_set_owned(pcb_solver *h, int64_t n_own);
 /* Device pointer and element count of a handle buffer (for collectives). */
+/* GPU-resident instance construction: the BASELINE synthetic
+ * grid built in HBM -- image of nshapes disks / balls (centres nshapes x ndim,
+ * radii, as instances.shapes_of draws them) plus the counter-based
+ * N(0, 0.15^2) noise of `seed`, unaries and edge weights with the BASELINE
+ * formulas, `integer` for the rounded variant, pairwise scale lam -- bit for
+ * bit the arrays of paracut_b200/instances.py.  Replaces GridEnergy +
+ * upload (graph.py:116-161) for generated instances. */
+int pcb_create_synthetic(const int64_t* dims, int ndim, int conn, int nshapes,
+                         const double* centres, const double* radii, uint64_t seed, double lam,
+                         int integer, int precision, int device, pcb_solver** out);
+/* The handle's instance back on the host (w: n doubles; dir_weights[k]: the
+ * direction arrays in graph.direction_shape order, as currently scaled; NULL
+ * entries skipped). */
+int pcb_get_instance(pcb_solver* h, double* w, double* const* dir_weights);
+
 /* Verified sweeps of the double-buffered fp32 step:
  * per family (r entries each, NULL allowed) the current mode (1 = the next
  * plain iteration verifies last iteration's segmentation, 0 = taut-string

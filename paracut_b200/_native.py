@@ -75,6 +75,9 @@ def _declare(L):
     L.pcb_set_profiling.argtypes = [P, INT]
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_verify_stats.argtypes = [P, P, P, P, P, P]
+    L.pcb_create_synthetic.argtypes = [P, INT, INT, INT, P, P, ctypes.c_uint64, ctypes.c_double,
+                                       INT, INT, INT, P]
+    L.pcb_get_instance.argtypes = [P, P, P]
     L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
     L.pcb_set_owned.argtypes = [P, I64]
     L.pcb_log_start.argtypes = [P]
@@ -97,7 +100,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
-           "pcb_log_jaccard", "pcb_verify_stats")
+           "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance")
 
 
 def lib():
@@ -200,6 +203,21 @@ class GridSolver:
         self.device = int(device)
         self.dims = tuple(int(d) for d in g.dims)
         dims = np.asarray(self.dims, dtype=np.int64)
+        if getattr(g, "_is_device_grid", False):
+            # GPU-resident construction: the generator builds the instance in HBM
+            h = P()
+            cen = _f64(g.centres.reshape(-1))
+            rad = _f64(g.radii)
+            check(L.pcb_create_synthetic(ptr(dims), len(self.dims), CONN_CODES[g.connectivity],
+                                         int(rad.size), ptr(cen), ptr(rad),
+                                         ctypes.c_uint64(int(g.seed)), float(g.lam),
+                                         int(bool(g.integer)), PRECISIONS[precision],
+                                         self.device, ctypes.byref(h)))
+            self._h = h
+            r, n = INT(0), I64(0)
+            check(L.pcb_shape(h, ctypes.byref(r), ctypes.byref(n)))
+            self.r, self.n = int(r.value), int(n.value)
+            return
         if getattr(g, "_is_grid_file", False):
             # device ingest: the payload goes file -> pinned staging -> HBM
             h = P()
@@ -420,6 +438,15 @@ class GridSolver:
 
     def set_profiling(self, on):
         check(lib().pcb_set_profiling(self.handle, int(bool(on))))
+
+    def get_instance(self, connectivity):
+        """(w, dir_weights) of the handle's instance, copied to the host."""
+        from .graph import DIRECTIONS, direction_shape
+        w = np.empty(self.n)
+        dws = [np.empty(direction_shape(self.dims, d)) for d in DIRECTIONS[connectivity]]
+        arr = (P * 4)(*([ptr(a) for a in dws] + [None] * (4 - len(dws))))
+        check(lib().pcb_get_instance(self.handle, ptr(w), arr))
+        return w, dws
 
     def verify_stats(self, scans=False):
         """(modes, verified sweeps, repaired chains[, scan sweeps, changed

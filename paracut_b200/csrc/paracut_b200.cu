@@ -385,6 +385,7 @@ __global__ void __launch_bounds__(FAM_BLOCK) k_tv1d(const double* s, const doubl
 
 #include "fast_sweep.cuh"
 #include "lean_verify.cuh"
+#include "generator.cuh"
 #include "exact_sweep.cuh"
 
 namespace {
@@ -1990,13 +1991,65 @@ int pcb_device_count(int* count) {
 
 namespace {
 
-// Weights source of a handle build: host arrays or a PCUT1B file.
+// Weights source of a handle build: host arrays, a PCUT1B file, or the
+// synthetic generator (built in HBM, generator.cuh).
+struct SynthSpec {
+  int nshapes = 0;
+  const double* centres = nullptr;  // nshapes x ndim
+  const double* radii = nullptr;
+  uint64_t seed = 0;
+  double lam = 1.0, sigma = 0.15, inv2s2 = 50.0, diag = 1.0;
+  int integer = 0;
+};
 struct WeightSource {
   const double* w = nullptr;
   const double* const* dirw = nullptr;
   int fd = -1;            // file: payload at `off` (w, then each direction array)
   int64_t off = 0;
+  const SynthSpec* syn = nullptr;
 };
+
+// the instance of a SynthSpec into h->w / h->dirw (stream 0, synchronous)
+int synth_build(pcb_solver* h, const SynthSpec& S) {
+  const int nd = h->D.nd;
+  DBuf<pcb::gen::Shape> shapes;
+  DBuf<uint8_t> mask;
+  if (int e = mask.alloc(h->n)) return e;
+  CUDA_TRY(cudaMemset(mask.p, 0, h->n));
+  if (S.nshapes > 0) {
+    std::vector<pcb::gen::Shape> hs(S.nshapes);
+    for (int b = 0; b < S.nshapes; ++b) {
+      for (int a = 0; a < 3; ++a) hs[b].c[a] = a < nd ? S.centres[b * nd + a] : 0.0;
+      hs[b].r = S.radii[b];
+    }
+    if (int e = shapes.alloc(S.nshapes)) return e;
+    CUDA_TRY(cudaMemcpy(shapes.p, hs.data(), hs.size() * sizeof(pcb::gen::Shape),
+                        cudaMemcpyHostToDevice));
+    pcb::gen::k_paint<<<S.nshapes, 256>>>(shapes.p, h->D, mask.p);
+    LAUNCH_CHECK(h);
+  }
+  const int g = grid_for(h->n, 256, 148 * 16);
+  pcb::gen::k_image<<<g, 256>>>(mask.p, h->n, S.seed, S.sigma, h->w.p);
+  LAUNCH_CHECK(h);
+  for (int k = 0; k < h->DG.ndir; ++k) {
+    const int64_t cnt = dir_size(h, k);
+    if (cnt <= 0) continue;
+    pcb::gen::EdgeArgs E{};
+    E.D = h->D;
+    for (int a = 0; a < 3; ++a) E.off[a] = h->DG.off[k][a];
+    E.count = cnt;
+    E.inv2s2 = S.inv2s2;
+    E.scale = (h->conn == PCB_CONN_2D8 && k >= 2) ? S.diag : 1.0;
+    E.lam = S.lam;
+    E.integer = S.integer;
+    pcb::gen::k_edges<<<grid_for(cnt, 256, 148 * 16), 256>>>(h->w.p, E, h->dirw[k].p);
+    LAUNCH_CHECK(h);
+  }
+  pcb::gen::k_unaries<<<g, 256>>>(h->w.p, h->n, S.integer);
+  LAUNCH_CHECK(h);
+  CUDA_TRY(cudaDeviceSynchronize());
+  return 0;
+}
 
 // pread `bytes` at `off` of fd into device memory through the pinned ring
 // (reads of chunk i+1 overlap the copy engine's chunk i).  nonneg: the payload
@@ -2095,14 +2148,16 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   setup_geometry(h);
   if ((rc = h->w.alloc(n))) return bail(rc);
   int64_t foff = src.off;
-  cudaError_t e = src.fd >= 0 ? file_h2d(h->w.p, src.fd, foff, n * sizeof(double), 0)
-                              : hostio::h2d(h->w.p, src.w, n * sizeof(double), 0);
+  cudaError_t e = cudaSuccess;
+  if (!src.syn)
+    e = src.fd >= 0 ? file_h2d(h->w.p, src.fd, foff, n * sizeof(double), 0)
+                    : hostio::h2d(h->w.p, src.w, n * sizeof(double), 0);
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "upload w: %s", cudaGetErrorString(e)));
   foff += n * (int64_t)sizeof(double);
   for (int k = 0; k < h->DG.ndir; ++k) {
     const int64_t cnt = dir_size(h, k);
     if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
-    if (cnt > 0) {
+    if (cnt > 0 && !src.syn) {
       if (src.fd >= 0) {
         bool neg = false;
         e = file_h2d(h->dirw[k].p, src.fd, foff, cnt * sizeof(double), 0, true, &neg);
@@ -2116,6 +2171,8 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
       foff += cnt * (int64_t)sizeof(double);
     }
   }
+  if (src.syn)
+    if ((rc = synth_build(h, *src.syn))) return bail(rc);
   phase("upload");
   const int64_t rn = (int64_t)h->r * n;
   if ((rc = h->y.alloc(rn))) return bail(rc);
@@ -2218,6 +2275,40 @@ int pcb_create_from_file(const char* path, int precision, int device, pcb_solver
   if (ndim_out) *ndim_out = ndim;
   if (conn_out) *conn_out = code;
   return create_impl(dims, ndim, code, precision, src, device, out);
+}
+
+int pcb_create_synthetic(const int64_t* dims, int ndim, int conn, int nshapes,
+                         const double* centres, const double* radii, uint64_t seed, double lam,
+                         int integer, int precision, int device, pcb_solver** out) {
+  if (!out || !dims || (nshapes > 0 && (!centres || !radii))) return fail(PCB_E_ARG, "null argument");
+  if (nshapes < 0) return fail(PCB_E_ARG, "negative shape count");
+  if (!(lam >= 0.0)) return fail(PCB_E_ARG, "scale factor must be nonnegative");
+  SynthSpec S;
+  S.nshapes = nshapes;
+  S.centres = centres;
+  S.radii = radii;
+  S.seed = seed;
+  S.lam = lam;
+  S.integer = integer ? 1 : 0;
+  S.sigma = 0.15;
+  S.inv2s2 = 1.0 / (2.0 * 0.1 * 0.1);  // instances.INV2S2
+  S.diag = 1.0 / sqrt(2.0);
+  WeightSource src;
+  src.syn = &S;
+  return create_impl(dims, ndim, conn, precision, src, device, out);
+}
+
+int pcb_get_instance(pcb_solver* h, double* w, double* const* dir_weights) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (int e = set_dev(h)) return e;
+  if (w) CUDA_TRY(hostio::d2h(w, h->w.p, h->n * sizeof(double), h->stream));
+  for (int k = 0; k < h->DG.ndir; ++k) {
+    const int64_t cnt = dir_size(h, k);
+    if (dir_weights && dir_weights[k] && cnt > 0)
+      CUDA_TRY(hostio::d2h(dir_weights[k], h->dirw[k].p, cnt * sizeof(double), h->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(h->stream));
+  return 0;
 }
 
 int pcb_debug_counters(uint64_t* out, int reset) {

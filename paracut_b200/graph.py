@@ -173,7 +173,8 @@ def instance_fingerprint(g):
 
 def as_grid(g):
     """Accept our GridEnergy or any object with the reference's grid fields."""
-    if isinstance(g, GridEnergy) or getattr(g, "_is_grid_file", False):
+    if (isinstance(g, GridEnergy) or getattr(g, "_is_grid_file", False)
+            or getattr(g, "_is_device_grid", False)):
         return g
     for attr in ("dims", "connectivity", "w", "dir_weights"):
         if not hasattr(g, attr):

@@ -356,7 +356,24 @@ def make_path():
         save("path_%s.npz" % name, **d)
 
 
-if __name__ == "__main__" and "path" in sys.argv[1:]:
+def make_cfg1():
+    """cfg1.npz alone: BASELINE cfg1 (256^2 2D-4, seed 0) through the reference
+    at k = 200 (rerun when the synthetic generator changes)."""
+    global _PC
+    pc = import_reference()
+    _PC = pc
+    sys.path.insert(0, REPO)
+    from paracut_b200.instances import make_instance
+    ours = make_instance("cfg1", seed=0)
+    g = pc.GridEnergy(ours.dims, ours.connectivity, ours.w, ours.dir_weights)
+    d = grid_arrays(g)
+    d.update(fixed_iter(pc, g, (200,)))
+    save("cfg1.npz", **d)
+
+
+if __name__ == "__main__" and "cfg1" in sys.argv[1:]:
+    make_cfg1()
+elif __name__ == "__main__" and "path" in sys.argv[1:]:
     make_path()
 elif __name__ == "__main__" and "io" in sys.argv[1:]:
     make_io()
