@@ -36,9 +36,12 @@ extern "C" {
  * PCB_F64: AAR point z kept in fp64 and updated with the reference's exact
  *          operation order -> iterates bitwise equal to solvers.py:289-298.
  * PCB_F32: shadow p_j stored fp32, shared drift c fp64, primal x fp32;
- *          z_j = p_j + c; all prox arithmetic in fp64 (SURVEY 8(a) a6 form). */
+ *          z_j = p_j + c; all prox arithmetic in fp64 (SURVEY 8(a) a6 form).
+ * PCB_F64S: the PCB_F32 form with fp64 state and fp64 scans, chains split at
+ *          merge points (not bitwise the reference; ~1e-12 relative). */
 #define PCB_F64 0
 #define PCB_F32 1
+#define PCB_F64S 2
 
 typedef struct pcb_solver pcb_solver;
 

@@ -21,7 +21,7 @@ STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
 BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_P, BUF_BITS = 0, 1, 2, 3, 4, 5, 6
 ALG_BCD, ALG_AP, ALG_FISTA = 1, 2, 3
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
-PRECISIONS = {"f64": 0, "f32": 1}
+PRECISIONS = {"f64": 0, "f32": 1, "f64s": 2}
 
 _lib = None
 _lock = threading.Lock()

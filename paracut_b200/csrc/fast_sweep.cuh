@@ -64,13 +64,16 @@ static_assert(TP == 8, "mode-B lane mapping assumes 8-position tiles");
 
 enum Role { FIRST = 0, MID = 1, LAST = 2, SHADOW = 3 };
 
-struct Args {
+// ST: storage type of the family state, weights, accumulator and primal --
+// float for the fp32-state mode, double for the fp64 split mode (f64s).
+template <class ST>
+struct ArgsT {
   Fam F;
-  float* p;         // family state, interleaved [pos][C]
-  const float* wf;  // family weights, interleaved [pos][C]
+  ST* p;            // family state, interleaved [pos][C]
+  const ST* wf;     // family weights, interleaved [pos][C]
   double* c;        // drift (natural node layout)
-  float* G;         // accumulator of p_new - p_old over families (natural)
-  float* X;         // primal x = w - sum_j p_j (natural)
+  ST* G;            // accumulator of p_new - p_old over families (natural)
+  ST* X;            // primal x = w - sum_j p_j (natural)
   double* y;        // SHADOW output (natural)
   double inv_r, rd;
   double* parts;    // per-block monitor partials
@@ -84,10 +87,10 @@ struct Args {
   // Double-buffered step (nullptr: in place).  The sweep reads p, c, X and
   // Gi and writes po, co, Xo and G, so its inputs stay intact for the local
   // repair of a verified sweep (VER) and for any other reader of the step.
-  float* po;        // new family state
+  ST* po;           // new family state
   double* co;       // LAST: new drift
-  float* Xo;        // LAST: new primal
-  const float* Gi;  // MID / LAST: accumulator in (G is the accumulator out)
+  ST* Xo;           // LAST: new primal
+  const ST* Gi;     // MID / LAST: accumulator in (G is the accumulator out)
   // Segment hints (SCAN writes, VER reads): per tile of TP positions one
   // uint16 per chain, [tile][C]; bit q: the left boundary of position
   // tile*TP+q is a ceiling touch (x rises), bit 8+q: a floor touch (x falls).
@@ -96,8 +99,12 @@ struct Args {
   int* vcount;      // SCAN: chains whose hints changed; VER: chains repaired
 };
 
+using Args = ArgsT<float>;
+using Args64 = ArgsT<double>;
+
 // in-place defaults for the double-buffer fields
-inline void args_inplace(Args& a) {
+template <class ST>
+inline void args_inplace(ArgsT<ST>& a) {
   if (!a.po) a.po = a.p;
   if (!a.co) a.co = a.c;
   if (!a.Xo) a.Xo = a.X;
@@ -164,6 +171,12 @@ __device__ __forceinline__ void cp8(void* dst, const void* src, bool pred) {
       " @p cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(s),
       "l"(src), "r"((int)pred));
 }
+// one state / weight element (4 or 8 bytes)
+template <class T>
+__device__ __forceinline__ void cp_elem(void* dst, const T* src, bool pred) {
+  if (sizeof(T) == 8) cp8(dst, src, pred);
+  else cp4(dst, src, pred);
+}
 __device__ __forceinline__ void l2_prefetch(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -212,19 +225,21 @@ __device__ __forceinline__ int pix(int l, int pos) {
   return r;
 }
 
-template <int ROLE>
+template <int ROLE, class ST = float>
 __host__ __device__ constexpr int ring_bytes_host() {
-  // rz f64, rp f32, ra f32 (SHADOW keeps its fp64 segment values split over
-  // the dead rp / ra slots), + NT tile mbarriers, padded
-  // to 128 B so every warp's tile slots stay TMA-aligned
-  return 32 * RL * (8 + 4 + 4) + 128;
+  // rz f64, rp / ra one state element each (an fp32 SHADOW keeps its fp64
+  // segment values split over the dead rp / ra slots), + NT tile mbarriers,
+  // padded to 128 B so every warp's tile slots stay TMA-aligned
+  return 32 * RL * (8 + 2 * (int)sizeof(ST)) + 128;
 }
 
 // lagging-lane accessors (positions below the ring), kept out of line
-__device__ __noinline__ double z_global(const Args& A, int64_t fi, int64_t nd) {
+template <class ST>
+__device__ __noinline__ double z_global(const ArgsT<ST>& A, int64_t fi, int64_t nd) {
   return (double)A.p[fi] + A.c[nd];
 }
-__device__ __noinline__ double a_global(const Args& A, int64_t fi) { return (double)A.wf[fi]; }
+template <class ST>
+__device__ __noinline__ double a_global(const ArgsT<ST>& A, int64_t fi) { return (double)A.wf[fi]; }
 
 // monitor terms with explicit FMAs (the TU is built with -fmad=false for the
 // exact path; the fp32-state monitor has no bitwise contract)
@@ -234,28 +249,28 @@ __device__ __forceinline__ double nrm_last(double dcv, double g, double rd, doub
   return __fma_rn(dcv, __fma_rn(rd, dcv, g + g), acc);
 }
 
-template <int ROLE>
-__device__ __noinline__ double finish_global(const Args& A, int64_t fi, int64_t nd, double fill) {
-  const float pold = A.p[fi];
+template <int ROLE, class ST>
+__device__ __noinline__ double finish_global(const ArgsT<ST>& A, int64_t fi, int64_t nd, double fill) {
+  const ST pold = A.p[fi];
   const double cz = A.c[nd];
   const double pn = ((double)pold + cz) - fill;
   if (ROLE == SHADOW) {
     A.y[nd] = pn;
     return 0.0;
   }
-  const float p32 = (float)pn;
+  const ST p32 = (ST)pn;
   const double d = (double)p32 - (double)pold;
   double nrm = nrm_d(d, 0.0);
   A.po[fi] = p32;
   if (ROLE == FIRST) {
-    A.G[nd] = (float)d;
+    A.G[nd] = (ST)d;
   } else if (ROLE == MID) {
-    A.G[nd] = (float)((double)A.Gi[nd] + d);
+    A.G[nd] = (ST)((double)A.Gi[nd] + d);
   } else {
-    const float g32 = (float)((double)A.Gi[nd] + d);
+    const ST g32 = (ST)((double)A.Gi[nd] + d);
     const double g = (double)g32;
     const double xn = (double)A.X[nd] - g;
-    A.Xo[nd] = (float)xn;
+    A.Xo[nd] = (ST)xn;
     const double dcv = (xn - g) * A.inv_r;
     A.co[nd] = cz + dcv;
     if (A.export_g) A.G[nd] = g32;
@@ -464,9 +479,11 @@ __device__ __noinline__ double repair_lane(const Args& A, int c32, int base32, i
   return nrm;
 }
 
-template <int ROLE, bool ROWLIKE, bool VER = false>
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float>
 __global__ void __launch_bounds__(WARPS * 32)
-    k_sweep(const __grid_constant__ Args A, const __grid_constant__ Maps M) {
+    k_sweep(const __grid_constant__ ArgsT<ST> A, const __grid_constant__ Maps M) {
+  static_assert(!VER || sizeof(ST) == 4, "verified sweeps run in the fp32-state mode");
+  constexpr bool S64 = sizeof(ST) == 8;  // fp64 state (f64s): fp64 scan, fp64 ring slots
   extern __shared__ __align__(128) unsigned char smem_raw[];  // TMA boxes land 128-B aligned
   // device-side choice between the two sweeps of a family (both are launched;
   // the one the mode word does not select returns at once)
@@ -477,10 +494,10 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int64_t c0 = ((int64_t)blockIdx.x * WARPS + wib) * 32;
   double nrm = 0.0;
 
-  unsigned char* base = smem_raw + (size_t)wib * ring_bytes_host<ROLE>();
+  unsigned char* base = smem_raw + (size_t)wib * ring_bytes_host<ROLE, ST>();
   double* rz = reinterpret_cast<double*>(base);
-  float* rp = reinterpret_cast<float*>(base + 32 * RL * 8);
-  float* ra = rp + 32 * RL;
+  ST* rp = reinterpret_cast<ST*>(base + 32 * RL * 8);
+  ST* ra = rp + 32 * RL;
   // ring layout: [pos][lane] rows of 32 for strided families (every access is
   // lane-contiguous, and a (positions x 32 chains) box is one contiguous
   // block); row-like families keep [lane][pos] with the XOR swizzle that
@@ -492,7 +509,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   auto tix = [&](int k0, int q) { return ROWLIKE ? rix(lane, k0 + q) : pix(lane, k0) + (q << 5); };
   const bool use_tma = !ROWLIKE && M.tma;
   unsigned long long* mbar =
-      reinterpret_cast<unsigned long long*>(base + 32 * RL * 16);
+      reinterpret_cast<unsigned long long*>(base + 32 * RL * (8 + 2 * sizeof(ST)));
 
   const bool warp_live = c0 < F.C;
   const int nvalid = warp_live ? (int)min((int64_t)32, F.C - c0) : 0;
@@ -556,7 +573,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   // in R = fp32 for the in-place roles (values are taken relative to the
   // anchor's z, so they stay O(|p| + local drift) and fp32 keeps ~1e-7 of
   // them) and in fp64 for the shadow, whose output feeds the certificates.
-  using R = typename std::conditional<ROLE == SHADOW, double, float>::type;
+  using R = typename std::conditional<ROLE == SHADOW || S64, double, float>::type;
+  // fp32-state SHADOW: its fp64 segment values are split over the rp / ra slots
+  constexpr bool QSPLIT = ROLE == SHADOW && !S64;
   // a lane is finished when its anchor reaches `stop` (lanes without a unit
   // have start = stop = 0); it is never active again, and its whole range
   // counts as emitted
@@ -589,7 +608,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   bool hchanged = false;
 
   // retire-only inputs prefetched into registers (G for MID/LAST, X for LAST)
-  float gpre[TP], xpre[TP];
+  ST gpre[TP], xpre[TP];
   int pre_tile = -1;
 
   int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
@@ -643,7 +662,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const unsigned bar = (unsigned)__cvta_generic_to_shared(&mbar[(T - t_first) & (NT - 1)]);
         const int slot = (T & (NT - 1)) * TP * 32;
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // ring was read generically
-        mbar_expect(bar, TP * 32 * (4 + 4 + 8));
+        mbar_expect(bar, TP * 32 * (2 * sizeof(ST) + 8));
         tma2d((unsigned)__cvta_generic_to_shared(rp + slot), &M.p, (int)c0, k0, bar);
         tma2d((unsigned)__cvta_generic_to_shared(ra + slot), &M.a, (int)c0, k0, bar);
         if (M.c3)
@@ -658,8 +677,8 @@ __global__ void __launch_bounds__(WARPS * 32)
       const int pos = k0 + q;
       const bool pr = valid && pos < m;
       const int fi = pr ? (pos * C32 + c32) : 0;
-      cp4(&rp[rx(lane, pos)], A.p + fi, pr);
-      cp4(&ra[rx(lane, pos)], A.wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
+      cp_elem(&rp[rx(lane, pos)], A.p + fi, pr);
+      cp_elem(&ra[rx(lane, pos)], A.wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
       if (!ROWLIKE) {
         const int nd = pr ? node(base32, pos) : 0;
         cp8(&rz[rx(lane, pos)], A.c + nd, pr);
@@ -691,8 +710,8 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int pos = k0 + q;
         const bool pr = valid && pos < m;
         const int nd = pr ? node(base32, pos) : 0;
-        gpre[q] = pr ? A.Gi[nd] : 0.f;
-        if (ROLE == LAST) xpre[q] = pr ? A.X[nd] : 0.f;
+        gpre[q] = pr ? A.Gi[nd] : ST(0);
+        if (ROLE == LAST) xpre[q] = pr ? A.X[nd] : ST(0);
       }
     } else {
       const int pos = k0 + (lane & 7);
@@ -702,8 +721,8 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int bi = bB[ib];
         const bool pr = i < nvalid && pos < m;
         const int nd = pr ? node(bi, pos) : 0;
-        gpre[ib] = pr ? A.Gi[nd] : 0.f;
-        if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : 0.f;
+        gpre[ib] = pr ? A.Gi[nd] : ST(0);
+        if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : ST(0);
       }
     }
   };
@@ -737,8 +756,10 @@ __global__ void __launch_bounds__(WARPS * 32)
         if ((stile >> q) & 1u) {
           zs = zj;
           // (SHADOW: the fp64 q split over the dead p / weight slots)
-          qs = (ROLE == SHADOW) ? __hiloint2double(__float_as_int(ra[ix]), __float_as_int(rp[ix]))
-                                : (double)ra[ix];
+          if (QSPLIT)
+            qs = __hiloint2double(__float_as_int((float)ra[ix]), __float_as_int((float)rp[ix]));
+          else
+            qs = (double)ra[ix];
           if (SGW) {
             // the segment's prox value; jumps below 1e-6 (fp32 rounding of q)
             // count as none, so the change count sees segmentation changes
@@ -754,29 +775,29 @@ __global__ void __launch_bounds__(WARPS * 32)
           if (!ROWLIKE) A.y[node(base32, pos)] = pn;
           else rz[ix] = pn;
         } else {
-          const float pold = rp[ix];
-          const float p32 = (float)pn;
+          const ST pold = rp[ix];
+          const ST p32 = (ST)pn;
           const double d = (double)p32 - (double)pold;
           nq = nrm_d(d, nq);
           A.po[(pos * C32 + c32)] = p32;
           if (!ROWLIKE) {
             const int nd = node(base32, pos);
             if (ROLE == FIRST) {
-              A.G[nd] = (float)d;
+              A.G[nd] = (ST)d;
             } else if (ROLE == MID) {
-              A.G[nd] = (float)((double)gpre[q] + d);
+              A.G[nd] = (ST)((double)gpre[q] + d);
             } else {
-              const float g32 = (float)((double)gpre[q] + d);
+              const ST g32 = (ST)((double)gpre[q] + d);
               const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
-              A.Xo[nd] = (float)xn;
+              A.Xo[nd] = (ST)xn;
               const double dcv = (xn - g) * A.inv_r;
               A.co[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
               if (A.export_g) A.G[nd] = g32;
               nq = nrm_last(dcv, g, A.rd, nq);
             }
           } else {
-            ra[ix] = (float)d;
+            ra[ix] = (ST)d;
           }
         }
       }
@@ -812,12 +833,12 @@ __global__ void __launch_bounds__(WARPS * 32)
           } else if (ROLE == FIRST) {
             A.G[nd] = ra[ix];
           } else if (ROLE == MID) {
-            A.G[nd] = (float)((double)gpre[ib] + (double)ra[ix]);
+            A.G[nd] = (ST)((double)gpre[ib] + (double)ra[ix]);
           } else {
-            const float g32 = (float)((double)gpre[ib] + (double)ra[ix]);
+            const ST g32 = (ST)((double)gpre[ib] + (double)ra[ix]);
             const double g = (double)g32;
             const double xn = (double)xpre[ib] - g;
-            A.Xo[nd] = (float)xn;
+            A.Xo[nd] = (ST)xn;
             const double dcv = (xn - g) * A.inv_r;
             A.co[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
             if (A.export_g) A.G[nd] = g32;
@@ -840,7 +861,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     // software-pipelined ring reads: the next gate's z and a are loaded at the
     // end of the previous trip (slots >= k are never written by the scan)
     double zn = rz[rx(lane, k)];
-    float an = ra[rx(lane, k)];
+    ST an = ra[rx(lane, k)];
     const int lim = min(avail_hi, stop);  // gates are consumed while k < lim
     // an anchor gate not consumed yet (unit start, or a restart whose gate
     // was not loaded when the string bent): t is its z
@@ -850,11 +871,11 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (act) {
         const int kp = k;
         double zabs = zn;
-        float af = an;
+        ST af = an;
         if (LAG && kp < lo_pos) {  // lagging lane below the ring
           const int fi = (kp * C32 + c32);
           zabs = z_global(A, fi, node(base32, kp));
-          af = kp < m - 1 ? (float)a_global(A, fi) : 0.f;
+          af = kp < m - 1 ? (ST)a_global(A, fi) : ST(0);
         }
         k = kp + 1;
         if (LAG) t = kp == i0 ? zabs : t;  // the anchor gate itself
@@ -865,7 +886,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         // a zero weight (or the unit end) makes this gate a mandatory piece end;
         // after an earlier bend the rescan reaches the same gate again, so no
         // piece-end state needs to be kept
-        const bool zw = !inner || af == 0.f;
+        const bool zw = !inner || af == ST(0);
         const R inv = rcp_r<R>(k - i0);
         Lc += cs;
         Lf += fs;
@@ -906,7 +927,7 @@ __global__ void __launch_bounds__(WARPS * 32)
           if (bk - 1 < lo_pos) ab = (R)a_global(A, ((bk - 1) * C32 + c32));
           const int e2 = min(min(bk, lo_pos), stop);
           for (int j = i0; j < e2; ++j)
-            nrm += finish_global<ROLE>(A, (j * C32 + c32), node(base32, j), fabs_);
+            nrm += finish_global<ROLE, ST>(A, (j * C32 + c32), node(base32, j), fabs_);
           s0 = e2;
           if (s0 < bk) qv = (R)((rz[rx(lane, s0)] - t) - (double)fill);
         }
@@ -914,12 +935,12 @@ __global__ void __launch_bounds__(WARPS * 32)
         const bool mark = LAG ? (bend && s0 < stop && s0 < bk) : bend;
         const int ixs = LAG ? rx(lane, s0) : ixi0;
         if (mark) {
-          if (ROLE == SHADOW) {  // fp64 q: low word in the p slot, high word in the weight slot
+          if (QSPLIT) {  // fp64 q: low word in the p slot, high word in the weight slot
             const double qd = (double)qv;
-            rp[ixs] = __int_as_float(__double2loint(qd));
-            ra[ixs] = __int_as_float(__double2hiint(qd));
+            rp[ixs] = (ST)__int_as_float(__double2loint(qd));
+            ra[ixs] = (ST)__int_as_float(__double2hiint(qd));
           }
-          else ra[ixs] = (float)qv;
+          else ra[ixs] = (ST)qv;
         }
         smask |= (unsigned)mark << (s0 & (RL - 1));
         // after a touch the string leaves the tube point: skr = -touch * a(bk-1)
@@ -946,7 +967,7 @@ __global__ void __launch_bounds__(WARPS * 32)
           // i.e. nearly every rescan.  Not at a zero weight or the unit end
           // (a mandatory piece end) or when position k is not loaded yet.
           const int k1 = k + 1;
-          const bool triv = bend && k < lim && k1 < stop && an != 0.f;
+          const bool triv = bend && k < lim && k1 < stop && an != ST(0);
           if (triv) {
             const R rk1 = (R)an;
             c0x = k1;
@@ -987,7 +1008,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   // segment that fails is still emitted; its lane is repaired after the sweep
   // (repair_lane: a taut string between true points around the failures).
   int ff = 0x7fffffff, fl = -1;  // VER: first failing segment start, last failing position
-  if (VER && warp_live && rhi > 0) {
+  if constexpr (VER) if (warp_live && rhi > 0) {
     constexpr float FINF = __builtin_huge_valf();
     bool vdone = !has;            // closed the chain's last segment, or abandoned
     double vt = 0.0, tp = 0.0;    // anchor (z at i0) of the open / previous segment
@@ -1120,7 +1141,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
     }
   }
-  if (VER) {
+  if constexpr (VER) {
     __syncwarp();  // the sweep's writes (mode-B lanes write other chains) are visible
     const bool dirty = valid && ff != 0x7fffffff;
 #ifndef PCB_NO_REPAIR  // timing experiments only: results are wrong without the repair
@@ -1156,13 +1177,13 @@ __global__ void __launch_bounds__(WARPS * 32)
 constexpr int MW = 16;
 __device__ __forceinline__ int mix(int l, int q) { return l * MW + (q ^ (l & (MW - 1))); }
 
-template <bool ROWLIKE>
-__global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, const float* wf,
+template <bool ROWLIKE, class ST = float>
+__global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const ST* p, const ST* wf,
                                                       const double* cdr, int lb, int nb, int window,
                                                       int* merge) {
   __shared__ double sz[MWARPS][32 * MW];
-  __shared__ float sa[MWARPS][32 * MW];
-  __shared__ float sp[MWARPS][32 * MW];
+  __shared__ ST sa[MWARPS][32 * MW];
+  __shared__ ST sp[MWARPS][32 * MW];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t c0 = ((int64_t)blockIdx.x * MWARPS + wib) * 32;
   const int b = blockIdx.y + 1;
@@ -1178,16 +1199,16 @@ __global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const float* p, co
   const int base = valid ? (int)fam_base(F, c) : 0;
   auto node = [&](int bb, int pos) { return bb + pos * ns32 + zz32 * ((pos + ph32) & 1); };
   double* z_s = sz[wib];
-  float* a_s = sa[wib];
-  float* p_s = sp[wib];
+  ST* a_s = sa[wib];
+  ST* p_s = sp[wib];
   // ---- stage positions [g, g + MW)
 #pragma unroll 4
   for (int q = 0; q < MW; ++q) {
     const int pos = g + q;
     const bool pr = valid && pos < m;
     const int fi = pr ? pos * C32 + c32 : 0;
-    cp4(&p_s[mix(lane, q)], p + fi, pr);
-    cp4(&a_s[mix(lane, q)], wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
+    cp_elem(&p_s[mix(lane, q)], p + fi, pr);
+    cp_elem(&a_s[mix(lane, q)], wf + (pos < m - 1 ? fi : 0), pr && pos < m - 1);
     if (!ROWLIKE) cp8(&z_s[mix(lane, q)], cdr + (pr ? node(base, pos) : 0), pr);
   }
   if (ROWLIKE) {

@@ -431,7 +431,8 @@ __global__ void k_init_exact(double* z, const double* w, int64_t n, int r) {
 
 // fp32 state from an fp64 z (natural [j][node]): c = mean_j z_j, p_j = z_j - c
 // stored chain-interleaved, x = w - sum_j p_j.
-__global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, const double* w,
+template <class ST>
+__global__ void k_set_fast(const double* z, ST* p, double* cdrift, ST* X, const double* w,
                            int64_t n, FamSet FS, Dims D) {
   const int r = FS.r;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -453,33 +454,35 @@ __global__ void k_set_fast(const double* z, float* p, double* cdrift, float* X, 
       int64_t c;
       int pos;
       if (!fam_index(FS.f[j], D, i, &c, &pos)) continue;  // zig-zag border: p = 0
-      const float pj = (float)(z[j * n + i] - m);
+      const ST pj = (ST)(z[j * n + i] - m);
       p[j * n + (int64_t)pos * FS.f[j].C + c] = pj;
       sp += (double)pj;
     }
     cdrift[i] = m;
-    X[i] = (float)(w[i] - sp);
+    X[i] = (ST)(w[i] - sp);
   }
 }
 
-__global__ void k_init_fast(float* p, double* cdrift, float* X, const double* w, int64_t n, int r) {
+template <class ST>
+__global__ void k_init_fast(ST* p, double* cdrift, ST* X, const double* w, int64_t n, int r) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    for (int j = 0; j < r; ++j) p[j * n + i] = 0.0f;
+    for (int j = 0; j < r; ++j) p[j * n + i] = ST(0);
     cdrift[i] = w[i] / (double)r;
-    X[i] = (float)w[i];
+    X[i] = (ST)w[i];
   }
 }
 
-__global__ void k_get_fast(const float* p, const double* cdrift, double* z, int64_t n, FamSet FS,
+template <class ST>
+__global__ void k_get_fast(const ST* p, const double* cdrift, double* z, int64_t n, FamSet FS,
                            Dims D) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     for (int j = 0; j < FS.r; ++j) {
       int64_t c;
       int pos;
-      const float pj = fam_index(FS.f[j], D, i, &c, &pos)
-                           ? p[j * n + (int64_t)pos * FS.f[j].C + c] : 0.0f;
+      const ST pj = fam_index(FS.f[j], D, i, &c, &pos)
+                           ? p[j * n + (int64_t)pos * FS.f[j].C + c] : ST(0);
       z[j * n + i] = (double)pj + cdrift[i];
     }
   }
@@ -501,10 +504,11 @@ __global__ void k_get_fast(const float* p, const double* cdrift, double* z, int6
 //                  to the 3D y permutation, so each node's update reads and
 //                  writes coalesced arrays only.
 // Same per-node arithmetic and family order as k_apply_fast.
+template <class ST>
 __global__ void __launch_bounds__(256) k_apply_rows(const double* __restrict__ y0,
-                                                    float* __restrict__ p0, float* __restrict__ G,
+                                                    ST* __restrict__ p0, ST* __restrict__ G,
                                                     int C, int L) {
-  __shared__ float tp[32][33];   // [pos][chain]: old state
+  __shared__ ST tp[32][33];   // [pos][chain]: old state
   __shared__ double ty[32][33];  // [chain][pos]: shadow
   const int tiles_c = (C + 31) / 32;
   const int tiles = tiles_c * ((L + 31) / 32);
@@ -515,7 +519,7 @@ __global__ void __launch_bounds__(256) k_apply_rows(const double* __restrict__ y
     for (int k = 0; k < 4; ++k) {
       const int r = ty8 + 8 * k;  // pos row for p, chain row for y
       const int pos = x0 + r, c = c0 + tx;
-      tp[r][tx] = (pos < L && c < C) ? p0[pos * C + c] : 0.f;
+      tp[r][tx] = (pos < L && c < C) ? p0[pos * C + c] : ST(0);
       const int cc = c0 + r, xx = x0 + tx;
       ty[r][tx] = (cc < C && xx < L) ? y0[cc * L + xx] : 0.0;
     }
@@ -526,21 +530,21 @@ __global__ void __launch_bounds__(256) k_apply_rows(const double* __restrict__ y
       const int cc = c0 + r, xx = x0 + tx;  // node (chain cc, pos xx)
       if (cc < C && xx < L) G[cc * L + xx] = tp[tx][r];
       const int pos = x0 + r, c = c0 + tx;  // family slot (pos, chain c)
-      if (pos < L && c < C) p0[pos * C + c] = (float)ty[tx][r];
+      if (pos < L && c < C) p0[pos * C + c] = (ST)ty[tx][r];
     }
     __syncthreads();
   }
 }
 
-template <int R>
+template <int R, class ST>
 __global__ void __launch_bounds__(256) k_apply_nodes(
-    const double* __restrict__ y, float* __restrict__ p, const float* __restrict__ G,
-    double* __restrict__ cdrift, float* __restrict__ X, const double* __restrict__ w, int n,
+    const double* __restrict__ y, ST* __restrict__ p, const ST* __restrict__ G,
+    double* __restrict__ cdrift, ST* __restrict__ X, const double* __restrict__ w, int n,
     int L, int D1, int C1, double* parts) {
   // rows of L nodes; 3D: row = z * D1 + y, family 1 (y lines) at [y][z][x]
   const int rows = n / L;
-  float* p1 = p + (int64_t)n;       // family 1 state
-  float* p2 = p + 2 * (int64_t)n;   // family 2 state (3D z lines: node order)
+  ST* p1 = p + (int64_t)n;       // family 1 state
+  ST* p2 = p + 2 * (int64_t)n;   // family 2 state (3D z lines: node order)
   const int lane = threadIdx.x & 31;
   const int wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nwg = gridDim.x * (blockDim.x >> 5);
@@ -551,7 +555,7 @@ __global__ void __launch_bounds__(256) k_apply_nodes(
     for (int x = lane; x < L; x += 32) {
       const int i = Rr * L + x;
       double yv[R];
-      float po[R];
+      ST po[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) yv[j] = y[(int64_t)j * n + i];
       po[0] = G[i];
@@ -561,7 +565,7 @@ __global__ void __launch_bounds__(256) k_apply_nodes(
       double g = 0.0, sp = 0.0;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const float pn = (float)yv[j];
+        const ST pn = (ST)yv[j];
         if (j == 1) p1[q1 + x] = pn;
         if (j == 2) p2[i] = pn;
         const double d = (double)pn - (double)po[j];
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(256) k_apply_nodes(
         acc += d * d;
       }
       const double xn = wi - sp;
-      X[i] = (float)xn;
+      X[i] = (ST)xn;
       const double dc = (xn - g) / (double)R;
       cdrift[i] = ci + dc;
       acc += 2.0 * dc * g + (double)R * dc * dc;
@@ -584,15 +588,15 @@ __global__ void __launch_bounds__(256) k_apply_nodes(
 constexpr int APPLY_TILE = 32;
 constexpr int APPLY_THREADS = 256;  // launch with exactly this many threads
 
-template <int R>
+template <int R, class ST>
 __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
-    const double* __restrict__ y, float* __restrict__ p, double* __restrict__ cdrift,
-    float* __restrict__ X, const double* __restrict__ w, int64_t n,
+    const double* __restrict__ y, ST* __restrict__ p, double* __restrict__ cdrift,
+    ST* __restrict__ X, const double* __restrict__ w, int64_t n,
     const __grid_constant__ FamSet FS, const __grid_constant__ Dims D, double* parts) {
   constexpr int T = APPLY_TILE, NW = APPLY_THREADS / 32;
   constexpr int CELLS = (T + 1) * T, PASSES = (CELLS + APPLY_THREADS - 1) / APPLY_THREADS;
   // chains R0-1 .. R0+T-1 (zig-zag chain c covers rows c and c+1) x T positions
-  __shared__ float tile[R][T + 1][T + 1];
+  __shared__ ST tile[R][T + 1][T + 1];
   const int64_t L = D.nd == 3 ? D.d[2] : D.d[1];
   const int64_t rows = n / L;
   const int64_t D1 = D.nd == 3 ? D.d[1] : 1;
@@ -608,13 +612,13 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
     for (int j = 0; j < R; ++j) {
       const Fam& F = FS.f[j];
       if (!fam_rowlike(F.kind)) continue;
-      float v[PASSES];
+      ST v[PASSES];
 #pragma unroll
       for (int k = 0; k < PASSES; ++k) {
         const int e = threadIdx.x + k * APPLY_THREADS;
         const int cc = e % (T + 1), xx = e / (T + 1);
         const int64_t c = R0 - 1 + cc, x = X0 + xx;
-        v[k] = (e < CELLS && c >= 0 && c < F.C && x < L) ? p[j * n + x * F.C + c] : 0.f;
+        v[k] = (e < CELLS && c >= 0 && c < F.C && x < L) ? p[j * n + x * F.C + c] : ST(0);
       }
 #pragma unroll
       for (int k = 0; k < PASSES; ++k) {
@@ -632,7 +636,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
 #pragma unroll 1
     for (int b0 = 0; b0 < T / NW; b0 += S) {
     double yv[S][R], wv[S], cv[S];
-    float po[S][R];
+    ST po[S][R];
     int qv[S][R];
     bool in[S][R];
 #pragma unroll
@@ -648,12 +652,12 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
           const int c = (F.kind == K_ZZ0 || F.kind == K_ZZ1) ? Rr - ((x + F.phase) & 1) : Rr;
           in[s][j] = ok && c >= 0 && c < F.C;  // zig-zag border node: not in this family
           qv[s][j] = c - ((int)R0 - 1);         // tile row
-          po[s][j] = in[s][j] ? tile[j][qv[s][j]][lane] : 0.f;
+          po[s][j] = in[s][j] ? tile[j][qv[s][j]][lane] : ST(0);
         } else {
           // COL2 / Z3: family layout == node order; Y3: [y][z][x]
           in[s][j] = ok;
           qv[s][j] = F.kind == K_Y3 ? (Rr % (int)D1) * (int)D0L + (Rr / (int)D1) * (int)L + x : i;
-          po[s][j] = ok ? p[(int64_t)j * n + qv[s][j]] : 0.f;
+          po[s][j] = ok ? p[(int64_t)j * n + qv[s][j]] : ST(0);
         }
       }
       wv[s] = ok ? w[i] : 0.0;
@@ -668,7 +672,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         if (!in[s][j]) continue;
-        const float pn = (float)yv[s][j];
+        const ST pn = (ST)yv[s][j];
         if (fam_rowlike(FS.f[j].kind)) tile[j][qv[s][j]][lane] = pn;
         else p[(int64_t)j * n + qv[s][j]] = pn;
         const double d = (double)pn - (double)po[s][j];
@@ -677,7 +681,7 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
         acc += d * d;
       }
       const double xn = wv[s] - sp;
-      X[i] = (float)xn;
+      X[i] = (ST)xn;
       const double dc = (xn - g) / (double)R;
       cdrift[i] = cv[s] + dc;
       acc += 2.0 * dc * g + (double)R * dc * dc;
@@ -1103,12 +1107,26 @@ struct pcb_solver {
   // these, then the two sets swap), per-family segment hints and the
   // per-family device mode words {mode (1 = VER), count}.
   bool dbuf = false;
-  int vtheta = 10;  // verify when fewer than vtheta % of a family's chains changed
+  // verify while fewer than vtheta % of a family's chains need a repair (the
+  // verified sweep's break-even on cfg5 is a few %: nearly every warp then
+  // holds a repairing lane)
+  int vtheta = 3;
   DBuf<float> p32b, G32b, X32b;
   DBuf<double> cdriftb;
   DBuf<uint16_t> sg[MAXR];
   DBuf<int> vstate;
   pcb::fast::Maps maps2[MAXR]{};  // TMA descriptors of the alternate buffers
+  // F64S (fp64 split mode): the fast path's state in fp64 (p, G, X; weights
+  // wf64), the same kernels with fp64 ring slots and fp64 scans
+  DBuf<double> p64, G64, X64;
+  pcb::fast::Maps maps64[MAXR]{};
+  // CUDA graphs of GRAPH_STEPS plain iterations (launch-bound small grids),
+  // one per buffer parity of the double-buffered step
+  int par = 0;  // swaps of the double-buffered state, mod 2
+  cudaStream_t gstream = nullptr;
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  int64_t glaunches[2] = {0, 0};  // kernel launches in each graph
+  DBuf<double> gnorms;
   int64_t merge_off[MAXR]{};
   // merges of a step run on a side stream, overlapping the sweeps (they
   // depend only on the state at the start of the step)
@@ -1131,7 +1149,7 @@ struct pcb_solver {
   pcb_solver() {
     bind(w, z, y, p32, cdrift, X32, G32, tmp, yprev, bits, xcur, bestlab, bestx, parts, vals,
          norms, sp_cx, sp_fx, sp_cy, sp_fy, packed, normlog, lablog, merge, p32b, G32b, X32b,
-         cdriftb, vstate);
+         cdriftb, vstate, p64, G64, X64, gnorms);
     bind_arr(sg);
     bind_arr(dirw);
     bind_arr(dirw_base);
@@ -1144,10 +1162,34 @@ struct pcb_solver {
     for (cudaEvent_t e : ev_merge)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    for (cudaGraphExec_t g : gexec)
+      if (g) cudaGraphExecDestroy(g);
+    if (gstream) cudaStreamDestroy(gstream);
   }
 };
 
 namespace {
+
+// The fast path's state of a handle by storage type: float for PCB_F32,
+// double for PCB_F64S (same kernels, templated on the type).
+template <class ST>
+struct FastState;
+template <>
+struct FastState<float> {
+  static float* p(pcb_solver* h) { return h->p32.p; }
+  static float* G(pcb_solver* h) { return h->G32.p; }
+  static float* X(pcb_solver* h) { return h->X32.p; }
+  static const float* wf(pcb_solver* h, int j) { return h->wf32[j].p; }
+  static pcb::fast::Maps* maps(pcb_solver* h) { return h->maps; }
+};
+template <>
+struct FastState<double> {
+  static double* p(pcb_solver* h) { return h->p64.p; }
+  static double* G(pcb_solver* h) { return h->G64.p; }
+  static double* X(pcb_solver* h) { return h->X64.p; }
+  static const double* wf(pcb_solver* h, int j) { return h->wf64[j].p; }
+  static pcb::fast::Maps* maps(pcb_solver* h) { return h->maps64; }
+};
 
 int set_dev(pcb_solver* h) {
   CUDA_TRY(cudaSetDevice(h->device));
@@ -1431,7 +1473,11 @@ int update_exact(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
+template <class ST>
 int apply_fast(pcb_solver* h, double* norm_slot) {
+  ST* const P = FastState<ST>::p(h);
+  ST* const Gb = FastState<ST>::G(h);
+  ST* const Xb = FastState<ST>::X(h);
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   const Fam* F = h->fam;
   const unsigned all = (1u << h->r) - 1u;
@@ -1440,16 +1486,16 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
                          (h->r == 3 && F[0].kind == K_X3 && F[1].kind == K_Y3 && F[2].kind == K_Z3));
   if (two_pass && getenv("PCB_APPLY_TILED") == nullptr) {
     const int C0 = (int)F[0].C, L = (int)F[0].m;  // rows of L nodes
-    k_apply_rows<<<NODE_GRID, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, C0, L);
+    k_apply_rows<<<NODE_GRID, 256, 0, h->stream>>>(h->y.p, P, Gb, C0, L);
     LAUNCH_CHECK(h);
     const int n = (int)h->n;
     const int D1 = h->r == 3 ? (int)h->D.d[1] : 1;
     const int C1 = h->r == 3 ? (int)(h->D.d[0] * h->D.d[2]) : 0;  // y family: [y][z][x]
     if (h->r == 2)
-      k_apply_nodes<2><<<g, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, h->cdrift.p, h->X32.p,
+      k_apply_nodes<2, ST><<<g, 256, 0, h->stream>>>(h->y.p, P, Gb, h->cdrift.p, Xb,
                                                 h->w.p, n, L, D1, C1, h->parts.p);
     else
-      k_apply_nodes<3><<<g, 256, 0, h->stream>>>(h->y.p, h->p32.p, h->G32.p, h->cdrift.p, h->X32.p,
+      k_apply_nodes<3, ST><<<g, 256, 0, h->stream>>>(h->y.p, P, Gb, h->cdrift.p, Xb,
                                                 h->w.p, n, L, D1, C1, h->parts.p);
     LAUNCH_CHECK(h);
     k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, norm_slot, 1);
@@ -1458,15 +1504,15 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   }
   switch (h->r) {
     case 2:
-      k_apply_fast<2><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+      k_apply_fast<2, ST><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, P, h->cdrift.p, Xb,
                                                       h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
     case 3:
-      k_apply_fast<3><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+      k_apply_fast<3, ST><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, P, h->cdrift.p, Xb,
                                                       h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
     default:
-      k_apply_fast<4><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->p32.p, h->cdrift.p, h->X32.p,
+      k_apply_fast<4, ST><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, P, h->cdrift.p, Xb,
                                                       h->w.p, h->n, famset(h), h->D, h->parts.p);
       break;
   }
@@ -1476,33 +1522,34 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
-template <int ROLE, bool ROWLIKE, bool VER = false>
-int launch_sweep(pcb_solver* h, const pcb::fast::Args& a_in, const pcb::fast::Maps& M) {
-  pcb::fast::Args a = a_in;
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float>
+int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fast::Maps& M) {
+  pcb::fast::ArgsT<ST> a = a_in;
   pcb::fast::args_inplace(a);
 #ifndef PCB_RING_PAD
 #define PCB_RING_PAD 0  // experiment knob: extra dynamic smem per block (occupancy probes)
 #endif
-  const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE>() + PCB_RING_PAD;
+  const int bytes = pcb::fast::WARPS * pcb::fast::ring_bytes_host<ROLE, ST>() + PCB_RING_PAD;
   // set once per device (outside any later CUDA-graph capture of the sweep)
   static unsigned set_mask = 0;
   const unsigned bit = 1u << (h->device & 31);
   if (!(set_mask & bit)) {
-    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER>,
+    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     set_mask |= bit;
   }
   const int per = pcb::fast::WARPS * 32;
   const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
-  pcb::fast::k_sweep<ROLE, ROWLIKE, VER><<<g, per, bytes, h->stream>>>(a, M);
+  pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST><<<g, per, bytes, h->stream>>>(a, M);
   LAUNCH_CHECK(h);
   return 0;
 }
 
-template <int ROLE>
-int launch_role(pcb_solver* h, const pcb::fast::Args& a, int j) {
-  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true>(h, a, h->maps[j])
-                               : launch_sweep<ROLE, false>(h, a, h->maps[j]);
+template <int ROLE, class ST>
+int launch_role(pcb_solver* h, const pcb::fast::ArgsT<ST>& a, int j) {
+  pcb::fast::Maps* M = FastState<ST>::maps(h);
+  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true, false, ST>(h, a, M[j])
+                               : launch_sweep<ROLE, false, false, ST>(h, a, M[j]);
 }
 
 // SCAN and VER sweeps of one family in the double-buffered step: both are
@@ -1528,8 +1575,11 @@ bool verify_ring() {
   return v == 1;
 }
 
-template <int ROLE>
-int launch_role_v(pcb_solver* h, const pcb::fast::Args& a, int j) {
+template <int ROLE, class ST>
+int launch_role_v(pcb_solver* h, const pcb::fast::ArgsT<ST>& a, int j) {
+  if constexpr (!std::is_same<ST, float>::value) {
+    return launch_role<ROLE, ST>(h, a, j);
+  } else {
   const bool rl = fam_rowlike(a.F.kind);
   if (int e = rl ? launch_sweep<ROLE, true>(h, a, h->maps[j]) : launch_sweep<ROLE, false>(h, a, h->maps[j]))
     return e;
@@ -1538,11 +1588,13 @@ int launch_role_v(pcb_solver* h, const pcb::fast::Args& a, int j) {
     return rl ? launch_sweep<ROLE, true, true>(h, a, h->maps[j])
               : launch_sweep<ROLE, false, true>(h, a, h->maps[j]);
   return rl ? launch_verify<ROLE, true>(h, a) : launch_verify<ROLE, false>(h, a);
+  }
 }
 
 // merge points of family j for the current state (before its sweep), on
 // stream st; a.merge / a.nb point the sweep at them
-int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a, cudaStream_t st) {
+template <class ST>
+int launch_merge(pcb_solver* h, int j, pcb::fast::ArgsT<ST>& a, cudaStream_t st) {
   a.merge = nullptr;
   a.nb = 1;
   if (h->nbk[j] <= 1) return 0;
@@ -1551,10 +1603,10 @@ int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a, cudaStream_t st) {
   const dim3 g((unsigned)((F.C + per - 1) / per), (unsigned)(h->nbk[j] - 1));
   int* out = h->merge.p + h->merge_off[j];
   if (fam_rowlike(F.kind))
-    pcb::fast::k_merge<true><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+    pcb::fast::k_merge<true, ST><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
                                                 4 * h->lbk[j], out);
   else
-    pcb::fast::k_merge<false><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
+    pcb::fast::k_merge<false, ST><<<g, per, 0, st>>>(F, a.p, a.wf, a.c, h->lbk[j], h->nbk[j],
                                                  4 * h->lbk[j], out);
   LAUNCH_CHECK(h);
   a.merge = out;
@@ -1562,7 +1614,8 @@ int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a, cudaStream_t st) {
   return 0;
 }
 
-int launch_merge(pcb_solver* h, int j, pcb::fast::Args& a) { return launch_merge(h, j, a, h->stream); }
+template <class ST>
+int launch_merge(pcb_solver* h, int j, pcb::fast::ArgsT<ST>& a) { return launch_merge(h, j, a, h->stream); }
 
 // side stream + events for the overlapped merges (created on first use)
 int ensure_side(pcb_solver* h) {
@@ -1599,7 +1652,10 @@ EncodeTiledFn encode_tiled() {
 // TMA maps for the strided families whose warps cover 32 consecutive nodes
 // (cols; 3D y with D2 % 32 == 0; 3D z).  Others keep the per-lane cp.async.
 // PCB_TMA=0 disables them.
-void build_maps_for(pcb_solver* h, float* pbuf, double* cbuf, pcb::fast::Maps* maps) {
+template <class ST>
+void build_maps_for(pcb_solver* h, ST* pbuf, double* cbuf, pcb::fast::Maps* maps) {
+  constexpr CUtensorMapDataType ET =
+      sizeof(ST) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   for (int j = 0; j < MAXR; ++j) maps[j] = pcb::fast::Maps{};
   const char* env = getenv("PCB_TMA");
   if (env && env[0] == '0') return;
@@ -1620,11 +1676,11 @@ void build_maps_for(pcb_solver* h, float* pbuf, double* cbuf, pcb::fast::Maps* m
     const cuuint32_t box2[2] = {32, (cuuint32_t)TP}, es2[2] = {1, 1};
     const cuuint64_t dp[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
     const cuuint64_t da[2] = {(cuuint64_t)F.C, (cuuint64_t)(F.m - 1)};
-    const cuuint64_t sp[1] = {(cuuint64_t)F.C * 4};
-    CUresult r1 = fn(&M.p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)(pbuf + (int64_t)j * h->n), dp, sp, box2, es2,
+    const cuuint64_t sp[1] = {(cuuint64_t)F.C * sizeof(ST)};
+    CUresult r1 = fn(&M.p, ET, 2, (void*)(pbuf + (int64_t)j * h->n), dp, sp, box2, es2,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    CUresult r2 = fn(&M.a, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)h->wf32[j].p, da, sp, box2,
+    CUresult r2 = fn(&M.a, ET, 2, (void*)FastState<ST>::wf(h, j), da, sp, box2,
                      es2, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     CUresult r3;
@@ -1650,6 +1706,10 @@ void build_maps_for(pcb_solver* h, float* pbuf, double* cbuf, pcb::fast::Maps* m
 }
 
 void build_maps(pcb_solver* h) {
+  if (h->precision == PCB_F64S) {
+    build_maps_for(h, h->p64.p, h->cdrift.p, h->maps64);
+    return;
+  }
   build_maps_for(h, h->p32.p, h->cdrift.p, h->maps);
   if (h->dbuf) build_maps_for(h, h->p32b.p, h->cdriftb.p, h->maps2);
 }
@@ -1664,7 +1724,7 @@ int fam_units(const pcb_solver* h, int j) {
 // chains, scan sweeps, changed chains} (int64) per family.
 constexpr int VS_FAM = 4;
 constexpr int VSTATE_INTS = VS_FAM * MAXR + 8 * MAXR;
-constexpr int VS_COOL0 = 12;  // plain iterations before the first verified probe
+constexpr int VS_COOL0 = 64;  // plain iterations before the first verified probe
 
 // Mode policy of the verified sweeps, once per double-buffered step (device
 // side, so graph-capturable and deterministic: it depends only on integer
@@ -1710,6 +1770,7 @@ void swap_buf(DBuf<T>& a, DBuf<T>& b) {
 
 // after a double-buffered step the alternate buffers hold the state
 void swap_state(pcb_solver* h) {
+  h->par ^= 1;
   swap_buf(h->p32, h->p32b);
   swap_buf(h->cdrift, h->cdriftb);
   swap_buf(h->X32, h->X32b);
@@ -1722,7 +1783,12 @@ void swap_state(pcb_solver* h) {
 // LAST role: the drift/primal update happens on another handle),
 // PCB_STEP_EXPORT_G (LAST stores its per-node g in G), PCB_STEP_NORM_RAW
 // (store the sum of squares, not its square root).
+template <class ST>
 int step_fast(pcb_solver* h, double* norm_slot, int flags) {
+  ST* const P = FastState<ST>::p(h);
+  ST* const G = FastState<ST>::G(h);
+  ST* const X = FastState<ST>::X(h);
+  constexpr bool F32 = std::is_same<ST, float>::value;
   const double inv_r = 1.0 / (double)h->r, rd = (double)h->r;
   int act[MAXR], na = 0;
   for (int q = 0; q < h->r; ++q) {
@@ -1731,8 +1797,7 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
   }
   const bool preset = flags & PCB_STEP_G_PRESET;
   const bool noupd = flags & PCB_STEP_NO_UPDATE;
-  if (na == 1 && !preset && !noupd) CUDA_TRY(cudaMemsetAsync(h->G32.p, 0, h->n * sizeof(float),
-                                                              h->stream));
+  if (na == 1 && !preset && !noupd) CUDA_TRY(cudaMemsetAsync(G, 0, h->n * sizeof(ST), h->stream));
   // Every merge depends only on the state at the start of the step (p_j, the
   // drift c, the weights): launch them all on the side stream now, so they
   // run in the earlier sweeps' tails; sweep j waits for merge j only.
@@ -1747,7 +1812,7 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
       for (int q = 0; q < na; ++q) {
         const int j = act[q];
         if (h->nbk[j] <= 1) continue;
-        pcb::fast::Args m{h->fam[j], h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p};
+        pcb::fast::ArgsT<ST> m{h->fam[j], P + (int64_t)j * h->n, FastState<ST>::wf(h, j), h->cdrift.p};
         if (int rc = launch_merge(h, j, m, h->side)) return rc;
         CUDA_TRY(cudaEventRecord(h->ev_merge[j], h->side));
         side_merge[j] = true;
@@ -1758,8 +1823,8 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
   // state, write the alternate buffers, swap at the end; families with segment
   // hints launch both the SCAN and the verified sweep (device mode word)
   const unsigned all = (1u << h->r) - 1u;
-  const bool dbuf = h->dbuf && flags == 0 && (h->fmask & all) == all && na == h->r && na >= 2;
-  float* Gb[2] = {h->G32.p, h->G32b.p};
+  const bool dbuf = F32 && h->dbuf && flags == 0 && (h->fmask & all) == all && na == h->r && na >= 2;
+  ST* Gb[2] = {G, (ST*)h->G32b.p};
   int gcur = 0;  // Gb[gcur]: the accumulator the previous role wrote
   int64_t off = 0;
   for (int q = 0; q < na; ++q) {
@@ -1769,13 +1834,13 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     if (q == na - 1 && !noupd) role = pcb::fast::LAST;
     else if (q == 0 && !preset && !(na == 1 && !noupd)) role = pcb::fast::FIRST;
     else role = pcb::fast::MID;
-    pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, h->G32.p,
-                      h->X32.p, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
-                      (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
+    pcb::fast::ArgsT<ST> a{F, P + (int64_t)j * h->n, FastState<ST>::wf(h, j), h->cdrift.p, G,
+                           X, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
+                           (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
     if (dbuf) {
-      a.po = h->p32b.p + (int64_t)j * h->n;
+      a.po = (ST*)h->p32b.p + (int64_t)j * h->n;
       a.co = h->cdriftb.p;
-      a.Xo = h->X32b.p;
+      a.Xo = (ST*)h->X32b.p;
       if (role == pcb::fast::FIRST) {  // G = d
         a.G = Gb[0];
         a.Gi = Gb[0];
@@ -1808,9 +1873,9 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     prof_begin(h, j);
     if (!side_merge[j]) rc = launch_merge(h, j, a);
     if (!rc) {
-      if (role == pcb::fast::FIRST) rc = launch_role_v<pcb::fast::FIRST>(h, a, j);
-      else if (role == pcb::fast::MID) rc = launch_role_v<pcb::fast::MID>(h, a, j);
-      else rc = launch_role_v<pcb::fast::LAST>(h, a, j);
+      if (role == pcb::fast::FIRST) rc = launch_role_v<pcb::fast::FIRST, ST>(h, a, j);
+      else if (role == pcb::fast::MID) rc = launch_role_v<pcb::fast::MID, ST>(h, a, j);
+      else rc = launch_role_v<pcb::fast::LAST, ST>(h, a, j);
     }
     prof_end(h);
     if (rc) return rc;
@@ -1850,14 +1915,16 @@ __global__ void k_apply_g(const float* g, float* X, double* cdr, int64_t n, int6
   if (threadIdx.x == 0) parts[blockIdx.x] = t;
 }
 
+template <class ST>
 int shadow_fast(pcb_solver* h) {
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
     if (F.C == 0 || !((h->fmask >> j) & 1u)) continue;
-    pcb::fast::Args a{F, h->p32.p + (int64_t)j * h->n, h->wf32[j].p, h->cdrift.p, nullptr,
+    pcb::fast::ArgsT<ST> a{F, FastState<ST>::p(h) + (int64_t)j * h->n, FastState<ST>::wf(h, j),
+                           h->cdrift.p, nullptr,
                       nullptr, h->y.p + (int64_t)j * h->n, 0.0, 0.0, h->parts.p, nullptr, 1, 0};
     if (int rc = launch_merge(h, j, a)) return rc;
-    if (int rc = launch_role<pcb::fast::SHADOW>(h, a, j)) return rc;
+    if (int rc = launch_role<pcb::fast::SHADOW, ST>(h, a, j)) return rc;
   }
   return 0;
 }
@@ -1868,13 +1935,17 @@ int choose_split(pcb_solver* h) {
   int64_t need = 0;
   const char* env = getenv("PCB_SPLIT_TARGET");  // tuning knob (warps)
   const int64_t target = env ? atoll(env) : 4096;
+  // shortest unit (positions): 16 for the fp64 split mode (its fp64 scan
+  // keeps merges reliable on short windows; measured on cfg1), 32 for fp32
+  const char* um = getenv("PCB_SPLIT_MIN");  // tuning knob
+  const int unit_min = um ? atoi(um) : (h->precision == PCB_F64S ? 16 : 32);
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
     const int64_t warps = (F.C + 31) / 32;
     int nb = 1;
-    if (F.C > 0 && warps < target && F.m >= 64) {
+    if (F.C > 0 && warps < target && F.m >= 2 * unit_min) {
       nb = (int)((target + warps - 1) / warps);
-      const int maxb = F.m / 32;
+      const int maxb = F.m / unit_min;
       if (nb > maxb) nb = maxb;
       if (nb < 1) nb = 1;
     }
@@ -1900,16 +1971,11 @@ int reset_verify(pcb_solver* h);
 
 int setup_verify(pcb_solver* h) {
   const char* env = getenv("PCB_VERIFY");
-  h->dbuf = !(env && env[0] == '0') && h->r >= 2;
-  if (!h->dbuf) return 0;
+  h->dbuf = false;
+  if ((env && env[0] == '0') || h->r < 2) return 0;
   const char* th = getenv("PCB_VERIFY_THETA");  // tuning / test knob (percent of chains)
-  h->vtheta = th ? atoi(th) : 10;
-  const int64_t rn = (int64_t)h->r * h->n;
-  if (int e = h->p32b.alloc(rn)) return e;
-  if (int e = h->cdriftb.alloc(h->n)) return e;
-  if (int e = h->X32b.alloc(h->n)) return e;
-  if (int e = h->G32b.alloc(h->n)) return e;
-  CUDA_TRY(cudaMemset(h->p32b.p, 0, rn * sizeof(float)));
+  h->vtheta = th ? atoi(th) : 3;
+  bool any = false;
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
     // row-like families only: their scan stages c through per-lane cp.async
@@ -1921,7 +1987,16 @@ int setup_verify(pcb_solver* h) {
     const int64_t cnt = (int64_t)((F.m + pcb::fast::TP - 1) / pcb::fast::TP) * F.C;
     if (int e = h->sg[j].alloc(cnt)) return e;
     CUDA_TRY(cudaMemset(h->sg[j].p, 0, cnt * sizeof(uint16_t)));
+    any = true;
   }
+  if (!any) return 0;  // nothing to verify: the single-buffer scan step
+  h->dbuf = true;
+  const int64_t rn = (int64_t)h->r * h->n;
+  if (int e = h->p32b.alloc(rn)) return e;
+  if (int e = h->cdriftb.alloc(h->n)) return e;
+  if (int e = h->X32b.alloc(h->n)) return e;
+  if (int e = h->G32b.alloc(h->n)) return e;
+  CUDA_TRY(cudaMemset(h->p32b.p, 0, rn * sizeof(float)));
   if (int e = h->vstate.alloc(VSTATE_INTS)) return e;
   CUDA_TRY(cudaMemset(h->vstate.p, 0, VSTATE_INTS * sizeof(int)));
   return reset_verify(h);
@@ -2107,7 +2182,7 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   if (conn < 0 || conn > 2) return fail(PCB_E_ARG, "unsupported connectivity code %d", conn);
   const int want_nd = conn == PCB_CONN_3D6 ? 3 : 2;
   if (ndim != want_nd) return fail(PCB_E_ARG, "dims rank does not match connectivity");
-  if (precision != PCB_F64 && precision != PCB_F32)
+  if (precision != PCB_F64 && precision != PCB_F32 && precision != PCB_F64S)
     return fail(PCB_E_ARG, "unknown precision %d", precision);
   // n < 2^31 is what the sweeps' 32-bit index math relies on; checked before
   // every multiply so a product of large dims cannot wrap first
@@ -2181,6 +2256,14 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   if (precision == PCB_F64) {
     if ((rc = h->z.alloc(rn))) return bail(rc);
     if ((rc = ensure_wf64(h))) return bail(rc);
+  } else if (precision == PCB_F64S) {  // the fast path in fp64 (no verified sweeps)
+    if ((rc = h->p64.alloc(rn))) return bail(rc);
+    if ((rc = h->cdrift.alloc(n))) return bail(rc);
+    if ((rc = h->X64.alloc(n))) return bail(rc);
+    if ((rc = h->G64.alloc(n))) return bail(rc);
+    if ((rc = ensure_wf64(h))) return bail(rc);
+    if ((rc = choose_split(h))) return bail(rc);
+    build_maps(h);
   } else {
     if ((rc = h->p32.alloc(rn))) return bail(rc);
     if ((rc = h->cdrift.alloc(n))) return bail(rc);
@@ -2435,6 +2518,8 @@ int pcb_init_cold(pcb_solver* h) {
   const int g = grid_for(h->n, 256, NODE_GRID);
   if (h->precision == PCB_F64) {
     k_init_exact<<<g, 256, 0, h->stream>>>(h->z.p, h->w.p, h->n, h->r);
+  } else if (h->precision == PCB_F64S) {
+    k_init_fast<<<g, 256, 0, h->stream>>>(h->p64.p, h->cdrift.p, h->X64.p, h->w.p, h->n, h->r);
   } else {
     k_init_fast<<<g, 256, 0, h->stream>>>(h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, h->r);
     if (int e = reset_verify(h)) return e;
@@ -2455,8 +2540,12 @@ int pcb_set_z(pcb_solver* h, const double* z) {
   } else {
     if (int e = h->tmp.alloc(rn)) return e;
     CUDA_TRY(hostio::h2d(h->tmp.p, z, rn * sizeof(double), h->stream));
-    k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
-        h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, famset(h), h->D);
+    if (h->precision == PCB_F64S)
+      k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+          h->tmp.p, h->p64.p, h->cdrift.p, h->X64.p, h->w.p, h->n, famset(h), h->D);
+    else
+      k_set_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+          h->tmp.p, h->p32.p, h->cdrift.p, h->X32.p, h->w.p, h->n, famset(h), h->D);
     LAUNCH_CHECK(h);
     if (int e = reset_verify(h)) return e;
   }
@@ -2476,9 +2565,12 @@ int pcb_get_z(pcb_solver* h, double* z) {
     CUDA_TRY(hostio::d2h(z, h->z.p, rn * sizeof(double), h->stream));
   } else {
     if (int e = h->tmp.alloc(rn)) return e;
-    k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->p32.p, h->cdrift.p,
-                                                                     h->tmp.p, h->n, famset(h),
-                                                                     h->D);
+    if (h->precision == PCB_F64S)
+      k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+          h->p64.p, h->cdrift.p, h->tmp.p, h->n, famset(h), h->D);
+    else
+      k_get_fast<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(
+          h->p32.p, h->cdrift.p, h->tmp.p, h->n, famset(h), h->D);
     LAUNCH_CHECK(h);
     CUDA_TRY(hostio::d2h(z, h->tmp.p, rn * sizeof(double), h->stream));
   }
@@ -2489,6 +2581,73 @@ int pcb_get_z(pcb_solver* h, double* z) {
 int pcb_aar_run(pcb_solver* h, int64_t iters, double* step_norms) {
   return pcb_aar_step(h, iters, 0, step_norms);
 }
+
+namespace {
+
+// one plain AAR iteration of any precision; its step norm into *slot
+int one_step(pcb_solver* h, double* slot, int flags) {
+  if (h->precision == PCB_F64) {
+    if (int rc = sweep_exact(h, h->z.p, h->y.p)) return rc;
+    return update_exact(h, slot);
+  }
+  if (h->precision == PCB_F64S) return step_fast<double>(h, slot, flags);
+  return step_fast<float>(h, slot, flags);
+}
+
+constexpr int GRAPH_STEPS = 8;  // even: the double-buffered state returns to its parity
+
+bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PCB_GRAPH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// GRAPH_STEPS iterations replayed from a CUDA graph captured on first use (the
+// step's launches -- sweeps, merges on the side stream, reductions, mode
+// words -- become one graph launch); norms land in h->gnorms.
+int graph_steps(pcb_solver* h) {
+  cudaGraphExec_t& ex = h->gexec[h->par];
+  if (!ex) {
+    if (!h->gstream) CUDA_TRY(cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+    if (!h->gnorms.p)
+      if (int e = h->gnorms.alloc(GRAPH_STEPS)) return e;
+    CUDA_TRY(cudaStreamSynchronize(h->stream));  // (capture runs nothing; order by sync)
+    const cudaStream_t keep = h->stream;
+    const int64_t launches = h->launches;
+    h->stream = h->gstream;
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
+    int rc = 0;
+    const int par0 = h->par;
+    for (int k = 0; k < GRAPH_STEPS && !rc; ++k) rc = one_step(h, h->gnorms.p + k, 0);
+    const cudaError_t ce = cudaStreamEndCapture(h->gstream, &graph);
+    h->stream = keep;
+    // capture swapped the host-side buffer roles GRAPH_STEPS times: back to par0
+    if (h->par != par0) return fail(PCB_E_STATE, "graph capture left the buffer parity");
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(PCB_E_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    const cudaError_t ie = cudaGraphInstantiate(&ex, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      ex = nullptr;
+      return fail(PCB_E_CUDA, "graph instantiate: %s", cudaGetErrorString(ie));
+    }
+    h->glaunches[h->par] = h->launches - launches;
+    h->launches = launches;  // (counted per replay below)
+  }
+  CUDA_TRY(cudaGraphLaunch(ex, h->stream));
+  h->launches += h->glaunches[h->par];
+  // the replay swapped the device buffers GRAPH_STEPS times (even): parity unchanged
+  return 0;
+}
+
+}  // namespace
 
 int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   if (!h) return fail(PCB_E_ARG, "null handle");
@@ -2505,15 +2664,16 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
     if (int e = grow_keep(h->normlog, (size_t)(h->nlog + iters), (size_t)h->nlog, h->stream, 4096))
       return e;
   double* nout = to_log ? h->normlog.p + h->nlog : h->norms.p;
-  for (int64_t k = 0; k < iters; ++k) {
-    int rc;
-    if (h->precision == PCB_F64) {
-      if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
-      if ((rc = update_exact(h, nout + k))) return rc;
-    } else {
-      if ((rc = step_fast(h, nout + k, flags))) return rc;
+  const bool use_graph = flags == 0 && !h->profiling && graphs_enabled() && h->precision != PCB_F64;
+  int64_t k = 0;
+  if (use_graph)
+    for (; k + GRAPH_STEPS <= iters; k += GRAPH_STEPS) {
+      if (int rc = graph_steps(h)) return rc;
+      CUDA_TRY(cudaMemcpyAsync(nout + k, h->gnorms.p, GRAPH_STEPS * sizeof(double),
+                               cudaMemcpyDeviceToDevice, h->stream));
     }
-  }
+  for (; k < iters; ++k)
+    if (int rc = one_step(h, nout + k, flags)) return rc;
   if (to_log) h->nlog += iters;
   h->have_shadow = false;
   h->y_valid = false;
@@ -2532,8 +2692,10 @@ int pcb_shadow(pcb_solver* h, double* y_out, double* s_out) {
   int rc;
   if (h->precision == PCB_F64) {
     if ((rc = sweep_exact(h, h->z.p, h->y.p))) return rc;
+  } else if (h->precision == PCB_F64S) {
+    if ((rc = shadow_fast<double>(h))) return rc;
   } else {
-    if ((rc = shadow_fast(h))) return rc;
+    if ((rc = shadow_fast<float>(h))) return rc;
   }
   h->have_shadow = true;
   h->y_valid = true;
@@ -2599,8 +2761,10 @@ int pcb_apply(pcb_solver* h, double* step_norm) {
   double* nout = to_log ? h->normlog.p + h->nlog : h->norms.p;
   if (h->precision == PCB_F64) {
     if ((rc = update_exact(h, nout))) return rc;
+  } else if (h->precision == PCB_F64S) {
+    if ((rc = apply_fast<double>(h, nout))) return rc;
   } else {
-    if ((rc = apply_fast(h, nout))) return rc;
+    if ((rc = apply_fast<float>(h, nout))) return rc;
   }
   if (to_log) h->nlog += 1;
   h->have_shadow = false;

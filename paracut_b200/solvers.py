@@ -13,7 +13,10 @@ result, trace, best-iterate, stopping and warm-start semantics
 Precision: ``SolverConfig.precision="f64"`` (default) keeps z in fp64 and
 reproduces the reference iterates bit for bit; ``"f32"`` stores the bounded
 shadows in fp32 with an fp64 drift vector (SURVEY 8(a) a6 fused form) and
-computes every prox in fp64 -- the fast path for large grids.
+computes every prox in fp64 -- the fast path for large grids; ``"f64s"`` is
+that fused form with fp64 state and fp64 scans, chains split at merge points
+(not bitwise, ~1e-12 relative to the reference) -- the fast fp64 path, and the
+one for small grids whose few chains leave the bitwise kernel latency bound.
 
 Extensions (defaults give the reference's behaviour): ``thresholds`` lists
 extra primal thresholds evaluated in the same pass; each check keeps the
@@ -41,7 +44,7 @@ from .projections import DualState
 
 ALGORITHMS = ("bcd", "ap", "aar", "fista")
 GAP_SLACK = 1e-6
-PRECISIONS = ("f64", "f32")
+PRECISIONS = ("f64", "f32", "f64s")
 MAX_THRESHOLDS = 8
 
 

@@ -190,3 +190,22 @@ def test_f32_warm_start_keeps_zigzag_border_nodes():
     S = _native.GridSolver(g, precision="f32")
     S.set_z(z)
     assert np.max(np.abs(S.get_z() - z)) <= 1e-6 * np.max(np.abs(z))
+
+
+@pytest.mark.parametrize("conn,dims,k", [("2D-4", (256, 256), 200), ("2D-8", (96, 80), 150),
+                                         ("3D-6", (24, 20, 28), 150)])
+def test_f64s_within_1e6_of_oracle(conn, dims, k):
+    """The fp64 split mode (fast kernels, fp64 state and scans, chains split
+    at merge points): within the north_star fp64 tolerance 1e-6 of the
+    reference at matched iterations (cfg1's geometry first)."""
+    from oracle import oracle as orc
+    spec = {"2D-4": CONFIGS["cfg1"], "2D-8": CONFIGS["cfg3"], "3D-6": CONFIGS["cfg4"]}[conn]
+    g = make_instance(spec, seed=5, dims=dims)
+    z_ref, y_ref, norms_ref = orc.aar(g, k, threads=8)
+    x_ref = g.w - y_ref.sum(axis=0)
+    res = pc.solve(g, pc.decompose_grid(g),
+                   pc.SolverConfig(max_iters=k, check_every=k + 1, precision="f64s"))
+    x = g.w - res.dual_state.y.sum(axis=0)
+    assert _rel(x, x_ref) <= 1e-6
+    assert _rel(res.dual_state.z, z_ref) <= 1e-6
+    assert np.allclose(res.monitor["aar_step_norm"], norms_ref, rtol=1e-6, atol=1e-9)

@@ -42,17 +42,18 @@ def test_verified_sweeps_match_oracle(dims, k, capsys):
 
 def test_forced_verification_with_stale_hints_is_exact(monkeypatch):
     """theta > 100 %: the verified family stays verified from its first probe
-    (iteration ~13) on, when the hints are far from the solution -- many
-    chains go through the repair, and the result still matches the oracle."""
+    (iteration ~65) on, when the hints are still far from the solution --
+    many chains go through the repair, and the result still matches the
+    oracle."""
     from oracle import oracle as orc
     monkeypatch.setenv("PCB_VERIFY_THETA", "1000")
     g = make_instance(CONFIGS["cfg4"], seed=3, dims=(12, 20, 36))
-    k = 60
+    k = 120
     _, y_ref, _ = orc.aar(g, k, threads=orc.max_threads())
     x_ref = g.w - y_ref.sum(axis=0)
     S, x = _run(g, k)
     modes, sweeps, rep = S.verify_stats()
-    assert sweeps.sum() >= k - 16
+    assert sweeps.sum() >= k - 70
     assert rep.sum() > 0
     assert _rel(x, x_ref) <= 1e-4
 
