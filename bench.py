@@ -224,15 +224,21 @@ def run_sharded(args, world, rank, local):
     import torch.distributed as dist
     from paracut_b200 import _native
     from paracut_b200.distributed import ShardedAAR, TorchComm
-    from paracut_b200.instances import CONFIGS, make_instance, algorithmic_bytes
+    from paracut_b200.graph import DIRECTIONS
+    from paracut_b200.instances import CONFIGS, DeviceGrid, HostPartsGrid, make_instance
 
     torch.cuda.set_device(local)
     if "MASTER_ADDR" not in os.environ:  # --sharded without torchrun: world of one
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29533", RANK="0", WORLD_SIZE="1")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = CONFIGS[args.workload]
-    g = make_instance(spec, seed=args.seed)
-    r, n = len(g.dir_weights), g.n
+    # every rank builds only its own slab and pencil: on its GPU for the timed
+    # run (pcb_create_synthetic_box), from host arrays of its parts for e2e;
+    # 2D-8 halo slabs fall back to the whole host instance
+    halo = spec.connectivity == "2D-8"
+    g = make_instance(spec, seed=args.seed) if halo else DeviceGrid(spec, seed=args.seed,
+                                                                    device=local)
+    r, n = len(DIRECTIONS[spec.connectivity]), int(np.prod(spec.dims))
     backend = lambda sub: _native.GridSolver(sub, precision="f32", device=local)
     sh = ShardedAAR(g, TorchComm(), [rank], backend, device="cuda")
     sh.init_cold()
@@ -287,8 +293,9 @@ def run_sharded(args, world, rank, local):
     # dominant family kernel on this rank (slab: local families, pencil: cross)
     pk, pk_kind = peaks()
     best = None
-    for h, (fms, fcnt), sub in zip(handles, prof, [sh.geo.slab_grid(g, rank),
-                                                 sh.geo.pencil_grid(g, rank)]):
+    subs = ([g.part(*d) for d in sh.geo.parts(rank)] if not halo
+            else [sh.geo.slab_grid(g, rank), sh.geo.pencil_grid(g, rank)])
+    for h, (fms, fcnt), sub in zip(handles, prof, subs):
         fe = _family_edges(sub)
         for j in range(len(fms)):
             if fcnt[j] and (best is None or fms[j] > best[0]):
@@ -303,7 +310,8 @@ def run_sharded(args, world, rank, local):
     torch.cuda.synchronize()
     dist.barrier()
     t0 = time.perf_counter()
-    sh2 = ShardedAAR(g, TorchComm(), [rank], backend, device="cuda")
+    g2 = g if halo else HostPartsGrid(spec, seed=args.seed, device=local)
+    sh2 = ShardedAAR(g2, TorchComm(), [rank], backend, device="cuda")
     sh2.init_cold()
     sh2.run(args.steps, norms=True)
     ys = sh2.local_shadow()
@@ -318,7 +326,8 @@ def run_sharded(args, world, rank, local):
            "h2d_bytes_per_step": world * h2d / args.steps,
            "d2h_bytes_per_step": world * d2h / args.steps, "wall_s": wall}
     if rank == 0:
-        B_iter = algorithmic_bytes(g, r, 4)
+        B_iter = 4 * ((2 * r + 1) * n + sum(int(np.prod([s - abs(o) for s, o in zip(spec.dims, d)]))
+                                           for d in DIRECTIONS[spec.connectivity]))
         line = {
             "metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,

@@ -139,6 +139,14 @@ int pcb_set_family_mask(pcb_solver *h, unsigned mask);
  * The LAST role's step-norm term sum(2 dc g + r dc^2) over the owned nodes
  * lands in norms[1] (PCB_BUF_NORMS). */
 int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
+/* The slab side of an overlapped sharded iteration in one pass: g = G + d_z
+ * with d_z received from the pencils (device float[P][dz][cp]), applied as
+ * pcb_apply_g does (norm term in norms[1]), and the new drift c written to
+ * the slab -> pencil send buffer (device double[P][dz][cp], the pencils' node
+ * order: they receive their drift instead of updating it).  Slabs without a
+ * halo row (3D-6, 2D-4). */
+int pcb_apply_g_exchange(pcb_solver *h, uintptr_t recv_dev, uintptr_t send_dev, int P, int dz,
+                         int cp);
 /* Nodes [n_own, n) of this handle are halo copies of nodes another shard
  * owns (2D-8 row slabs carry the next slab's first row for the zig-zag path
  * that straddles the boundary): pcb_check labels them (their edges to owned
@@ -156,6 +164,16 @@ int pcb_set_owned(pcb_solver *h, int64_t n_own);
 int pcb_create_synthetic(const int64_t* dims, int ndim, int conn, int nshapes,
                          const double* centres, const double* radii, uint64_t seed, double lam,
                          int integer, int precision, int device, pcb_solver** out);
+/* The same for a box [origin, origin + extent) of the global grid gdims (a
+ * rank's z-slab or pencil in a sharded run): the handle has `dims` (the box's
+ * nodes in C order, possibly flattened), node values from global coordinates
+ * and global noise indices, the box's internal edges for the directions in
+ * dir_mask (bit k = DIRECTIONS[conn][k]) and zero weights elsewhere. */
+int pcb_create_synthetic_box(const int64_t* gdims, int ndim, int conn, const int64_t* origin,
+                             const int64_t* extent, const int64_t* dims, unsigned dir_mask,
+                             int nshapes, const double* centres, const double* radii,
+                             uint64_t seed, double lam, int integer, int precision, int device,
+                             pcb_solver** out);
 /* The handle's instance back on the host (w: n doubles; dir_weights[k]: the
  * direction arrays in graph.direction_shape order, as currently scaled; NULL
  * entries skipped). */

@@ -75,9 +75,12 @@ def _declare(L):
     L.pcb_set_profiling.argtypes = [P, INT]
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_verify_stats.argtypes = [P, P, P, P, P, P]
+    L.pcb_apply_g_exchange.argtypes = [P, ctypes.c_size_t, ctypes.c_size_t, INT, INT, INT]
     L.pcb_create_synthetic.argtypes = [P, INT, INT, INT, P, P, ctypes.c_uint64, ctypes.c_double,
                                        INT, INT, INT, P]
     L.pcb_get_instance.argtypes = [P, P, P]
+    L.pcb_create_synthetic_box.argtypes = [P, INT, INT, P, P, P, ctypes.c_uint, INT, P, P,
+                                           ctypes.c_uint64, ctypes.c_double, INT, INT, INT, P]
     L.pcb_jaccard_packed.argtypes = [P, P, I64, DBL_P]
     L.pcb_set_owned.argtypes = [P, I64]
     L.pcb_log_start.argtypes = [P]
@@ -100,7 +103,8 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_get_best", "pcb_level_set", "pcb_dual_init", "pcb_dual_run", "pcb_release_memory", "pcb_create_from_file", "pcb_scale_pairwise", "pcb_debug_counters", "pcb_project_K", "pcb_project_L", "pcb_set_profiling", "pcb_profile_read", "pcb_launch_count",
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
-           "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance")
+           "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance",
+           "pcb_apply_g_exchange", "pcb_create_synthetic_box")
 
 
 def lib():
@@ -208,11 +212,22 @@ class GridSolver:
             h = P()
             cen = _f64(g.centres.reshape(-1))
             rad = _f64(g.radii)
-            check(L.pcb_create_synthetic(ptr(dims), len(self.dims), CONN_CODES[g.connectivity],
-                                         int(rad.size), ptr(cen), ptr(rad),
-                                         ctypes.c_uint64(int(g.seed)), float(g.lam),
-                                         int(bool(g.integer)), PRECISIONS[precision],
-                                         self.device, ctypes.byref(h)))
+            box = getattr(g, "box", None)
+            if box is None:
+                check(L.pcb_create_synthetic(ptr(dims), len(self.dims), CONN_CODES[g.connectivity],
+                                             int(rad.size), ptr(cen), ptr(rad),
+                                             ctypes.c_uint64(int(g.seed)), float(g.lam),
+                                             int(bool(g.integer)), PRECISIONS[precision],
+                                             self.device, ctypes.byref(h)))
+            else:
+                gd, org, ext, mask = box
+                gd, org, ext = (np.asarray(v, dtype=np.int64) for v in (gd, org, ext))
+                check(L.pcb_create_synthetic_box(ptr(gd), len(gd), CONN_CODES[g.connectivity],
+                                                 ptr(org), ptr(ext), ptr(dims), int(mask),
+                                                 int(rad.size), ptr(cen), ptr(rad),
+                                                 ctypes.c_uint64(int(g.seed)), float(g.lam),
+                                                 int(bool(g.integer)), PRECISIONS[precision],
+                                                 self.device, ctypes.byref(h)))
             self._h = h
             r, n = INT(0), I64(0)
             check(L.pcb_shape(h, ctypes.byref(r), ctypes.byref(n)))
@@ -296,6 +311,11 @@ class GridSolver:
 
     def apply_g(self, g_dev_ptr):
         check(lib().pcb_apply_g(self.handle, int(g_dev_ptr)))
+
+    def apply_g_exchange(self, recv_ptr, send_ptr, P, dz, cp):
+        """g = G + received d_z, into the send buffer and applied (pcb_apply_g_exchange)."""
+        check(lib().pcb_apply_g_exchange(self.handle, int(recv_ptr), int(send_ptr), int(P),
+                                         int(dz), int(cp)))
 
     def set_owned(self, n_own):
         """Nodes [n_own, n) are halo copies owned by another shard (pcb_set_owned)."""

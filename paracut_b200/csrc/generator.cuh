@@ -132,15 +132,38 @@ struct Shape {
   double r;
 };
 
-// mark the nodes of one disk / ball (block = shape, threads stride its box)
-__global__ void k_paint(const Shape* shapes, Dims D, uint8_t* mask) {
+// The generated region: a box [o, o + e) of the global grid G (per axis); its
+// nodes in C order are the handle's nodes (the handle's dims may flatten the
+// box, e.g. a z-slab pencil (D0, 1, cp) of the box (D0, D1 / P, D2)).
+struct Box {
+  Dims G;          // global grid
+  int64_t o[3], e[3];
+  int64_t nb;      // nodes in the box
+};
+
+__device__ __forceinline__ void box_coords(const Box& B, int64_t t, int64_t idx[3]) {
+  int64_t rem = t;
+  for (int a = B.G.nd - 1; a >= 0; --a) {
+    idx[a] = B.o[a] + rem % B.e[a];
+    rem /= B.e[a];
+  }
+}
+__device__ __forceinline__ int64_t global_index(const Box& B, const int64_t idx[3]) {
+  int64_t g = 0;
+  for (int a = 0; a < B.G.nd; ++a) g = g * B.G.d[a] + idx[a];
+  return g;
+}
+
+// mark the box nodes of one disk / ball (block = shape, threads stride its box)
+__global__ void k_paint(const Shape* shapes, Box B, uint8_t* mask) {
   const Shape S = shapes[blockIdx.x];
-  const int nd = D.nd;
+  const int nd = B.G.nd;
   int64_t lo[3] = {0, 0, 0}, ext[3] = {1, 1, 1};
   int64_t vol = 1;
   for (int a = 0; a < nd; ++a) {
-    const int64_t l = max((int64_t)0, (int64_t)floor(S.c[a] - S.r));
-    const int64_t h = min(D.d[a], (int64_t)ceil(S.c[a] + S.r) + 1);
+    // the shape's box (instances.synth_image), cut to the generated box
+    const int64_t l = max(max((int64_t)0, (int64_t)floor(S.c[a] - S.r)), B.o[a]);
+    const int64_t h = min(min(B.G.d[a], (int64_t)ceil(S.c[a] + S.r) + 1), B.o[a] + B.e[a]);
     if (h <= l) return;
     lo[a] = l;
     ext[a] = h - l;
@@ -159,43 +182,45 @@ __global__ void k_paint(const Shape* shapes, Dims D, uint8_t* mask) {
       d2 = d2 + dx * dx;
     }
     if (d2 <= r2) {
-      int64_t nd_ = 0;
-      for (int a = 0; a < nd; ++a) nd_ = nd_ * D.d[a] + idx[a];
-      mask[nd_] = 1;
+      int64_t loc = 0;
+      for (int a = 0; a < nd; ++a) loc = loc * B.e[a] + (idx[a] - B.o[a]);
+      mask[loc] = 1;
     }
   }
 }
 
-// image, then the unaries w (in place of the image) after the edge weights
-__global__ void k_image(const uint8_t* mask, int64_t n, uint64_t seed, double sigma, double* img) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    img[i] = (mask[i] ? 0.7 : 0.3) + sigma * noise(seed, i);
+// image of the box nodes (noise counter = global node index)
+__global__ void k_image(const uint8_t* mask, Box B, uint64_t seed, double sigma, double* img) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < B.nb;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t idx[3];
+    box_coords(B, t, idx);
+    img[t] = (mask[t] ? 0.7 : 0.3) + sigma * noise(seed, global_index(B, idx));
+  }
 }
 
 struct EdgeArgs {
-  Dims D;
-  int off[3];      // direction d
-  int64_t count;   // elements of direction_shape(dims, d)
+  int off[3];      // direction d (global axes)
+  int64_t count;   // d-edges inside the box, C order of the box's direction shape
   double inv2s2, scale, lam;
   int integer;
 };
 
-__global__ void k_edges(const double* img, EdgeArgs E, double* out) {
-  const Dims& D = E.D;
+// the d-edges between two box nodes (both ends inside the box)
+__global__ void k_edges(const double* img, Box B, EdgeArgs E, double* out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E.count;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t rem = e, ja[3] = {0, 0, 0};
-    for (int a = D.nd - 1; a >= 0; --a) {
-      const int64_t ext = D.d[a] - (E.off[a] < 0 ? -E.off[a] : E.off[a]);
+    for (int a = B.G.nd - 1; a >= 0; --a) {
+      const int64_t ext = B.e[a] - (E.off[a] < 0 ? -E.off[a] : E.off[a]);
       ja[a] = rem % ext;
       rem /= ext;
     }
     int64_t na = 0, nb = 0;
-    for (int a = 0; a < D.nd; ++a) {
+    for (int a = 0; a < B.G.nd; ++a) {
       const int k = E.off[a];
-      na = na * D.d[a] + ja[a] + (k < 0 ? -k : 0);
-      nb = nb * D.d[a] + ja[a] + (k >= 0 ? k : 0);
+      na = na * B.e[a] + ja[a] + (k < 0 ? -k : 0);
+      nb = nb * B.e[a] + ja[a] + (k >= 0 ? k : 0);
     }
     const double diff = img[na] - img[nb];
     double v = series_exp(-(diff * diff) * E.inv2s2);

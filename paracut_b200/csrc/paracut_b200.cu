@@ -2075,6 +2075,11 @@ struct SynthSpec {
   uint64_t seed = 0;
   double lam = 1.0, sigma = 0.15, inv2s2 = 50.0, diag = 1.0;
   int integer = 0;
+  // the generated box of the global grid (default: the whole handle grid);
+  // dir_mask: directions generated (others zero, e.g. a pencil's non-cross ones)
+  bool box = false;
+  int64_t gdims[3] = {1, 1, 1}, origin[3] = {0, 0, 0}, extent[3] = {1, 1, 1};
+  unsigned dir_mask = 0xfu;
 };
 struct WeightSource {
   const double* w = nullptr;
@@ -2087,6 +2092,16 @@ struct WeightSource {
 // the instance of a SynthSpec into h->w / h->dirw (stream 0, synchronous)
 int synth_build(pcb_solver* h, const SynthSpec& S) {
   const int nd = h->D.nd;
+  pcb::gen::Box B{};
+  B.G = h->D;
+  B.nb = 1;
+  for (int a = 0; a < 3; ++a) {
+    B.G.d[a] = S.box ? S.gdims[a] : h->D.d[a];
+    B.o[a] = S.box ? S.origin[a] : 0;
+    B.e[a] = S.box ? S.extent[a] : h->D.d[a];
+    if (a < nd) B.nb *= B.e[a];
+  }
+  if (B.nb != h->n) return fail(PCB_E_ARG, "generated box does not match the handle's nodes");
   DBuf<pcb::gen::Shape> shapes;
   DBuf<uint8_t> mask;
   if (int e = mask.alloc(h->n)) return e;
@@ -2100,24 +2115,32 @@ int synth_build(pcb_solver* h, const SynthSpec& S) {
     if (int e = shapes.alloc(S.nshapes)) return e;
     CUDA_TRY(cudaMemcpy(shapes.p, hs.data(), hs.size() * sizeof(pcb::gen::Shape),
                         cudaMemcpyHostToDevice));
-    pcb::gen::k_paint<<<S.nshapes, 256>>>(shapes.p, h->D, mask.p);
+    pcb::gen::k_paint<<<S.nshapes, 256>>>(shapes.p, B, mask.p);
     LAUNCH_CHECK(h);
   }
   const int g = grid_for(h->n, 256, 148 * 16);
-  pcb::gen::k_image<<<g, 256>>>(mask.p, h->n, S.seed, S.sigma, h->w.p);
+  pcb::gen::k_image<<<g, 256>>>(mask.p, B, S.seed, S.sigma, h->w.p);
   LAUNCH_CHECK(h);
   for (int k = 0; k < h->DG.ndir; ++k) {
     const int64_t cnt = dir_size(h, k);
     if (cnt <= 0) continue;
+    if (!((S.dir_mask >> k) & 1u)) {
+      CUDA_TRY(cudaMemset(h->dirw[k].p, 0, cnt * sizeof(double)));
+      continue;
+    }
     pcb::gen::EdgeArgs E{};
-    E.D = h->D;
-    for (int a = 0; a < 3; ++a) E.off[a] = h->DG.off[k][a];
+    int64_t bcnt = 1;  // the direction's edges inside the box
+    for (int a = 0; a < 3; ++a) {
+      E.off[a] = h->DG.off[k][a];
+      if (a < nd) bcnt *= std::max<int64_t>(B.e[a] - (E.off[a] < 0 ? -E.off[a] : E.off[a]), 0);
+    }
+    if (bcnt != cnt) return fail(PCB_E_ARG, "generated box edges do not match direction %d", k);
     E.count = cnt;
     E.inv2s2 = S.inv2s2;
     E.scale = (h->conn == PCB_CONN_2D8 && k >= 2) ? S.diag : 1.0;
     E.lam = S.lam;
     E.integer = S.integer;
-    pcb::gen::k_edges<<<grid_for(cnt, 256, 148 * 16), 256>>>(h->w.p, E, h->dirw[k].p);
+    pcb::gen::k_edges<<<grid_for(cnt, 256, 148 * 16), 256>>>(h->w.p, B, E, h->dirw[k].p);
     LAUNCH_CHECK(h);
   }
   pcb::gen::k_unaries<<<g, 256>>>(h->w.p, h->n, S.integer);
@@ -2375,6 +2398,38 @@ int pcb_create_synthetic(const int64_t* dims, int ndim, int conn, int nshapes,
   S.integer = integer ? 1 : 0;
   S.sigma = 0.15;
   S.inv2s2 = 1.0 / (2.0 * 0.1 * 0.1);  // instances.INV2S2
+  S.diag = 1.0 / sqrt(2.0);
+  WeightSource src;
+  src.syn = &S;
+  return create_impl(dims, ndim, conn, precision, src, device, out);
+}
+
+int pcb_create_synthetic_box(const int64_t* gdims, int ndim, int conn, const int64_t* origin,
+                             const int64_t* extent, const int64_t* dims, unsigned dir_mask,
+                             int nshapes, const double* centres, const double* radii,
+                             uint64_t seed, double lam, int integer, int precision, int device,
+                             pcb_solver** out) {
+  if (!out || !gdims || !origin || !extent || !dims || (nshapes > 0 && (!centres || !radii)))
+    return fail(PCB_E_ARG, "null argument");
+  if (ndim < 2 || ndim > 3) return fail(PCB_E_ARG, "dims rank must be 2 or 3");
+  SynthSpec S;
+  for (int a = 0; a < ndim; ++a) {
+    if (origin[a] < 0 || extent[a] < 1 || origin[a] + extent[a] > gdims[a])
+      return fail(PCB_E_ARG, "box [origin, origin + extent) outside the grid on axis %d", a);
+    S.gdims[a] = gdims[a];
+    S.origin[a] = origin[a];
+    S.extent[a] = extent[a];
+  }
+  S.box = true;
+  S.dir_mask = dir_mask;
+  S.nshapes = nshapes;
+  S.centres = centres;
+  S.radii = radii;
+  S.seed = seed;
+  S.lam = lam;
+  S.integer = integer ? 1 : 0;
+  S.sigma = 0.15;
+  S.inv2s2 = 1.0 / (2.0 * 0.1 * 0.1);
   S.diag = 1.0 / sqrt(2.0);
   WeightSource src;
   src.syn = &S;
@@ -3120,6 +3175,56 @@ int pcb_apply_g(pcb_solver* h, uintptr_t g_dev) {
   k_apply_g<<<g, 256, 0, h->stream>>>(reinterpret_cast<const float*>(g_dev), h->X32.p,
                                       h->cdrift.p, h->n, h->n_own < 0 ? h->n : h->n_own,
                                       1.0 / (double)h->r, (double)h->r, h->parts.p);
+  LAUNCH_CHECK(h);
+  k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p + 1, 0);
+  LAUNCH_CHECK(h);
+  return 0;
+}
+
+// Slab side of a sharded iteration, fused (distributed.py overlapped
+// schedule): g = G + d_z (the cross family's d received in the pencil ->
+// slab exchange, layout [P][dz][cp]), the drift / primal update x -= g,
+// c += (x - g) / r, and the new drift straight into the slab -> pencil send
+// buffer (same layout, which is the pencils' node order) -- one pass instead
+// of a transposed add, a transposed copy and apply_g, and no update pass on
+// the pencils (they receive their drift).
+__global__ void k_apply_g_xchg(const float* __restrict__ G, const float* __restrict__ recv,
+                               double* __restrict__ send, float* __restrict__ X,
+                               double* __restrict__ cdr, int ns, int plane, int dz, int cp,
+                               double inv_r, double rd, double* parts) {
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+    const int zr = i / plane, col = i - zr * plane;
+    const int q = col / cp, cc = col - q * cp;
+    const int t = (q * dz + zr) * cp + cc;
+    const float g32 = G[i] + recv[t];
+    const double gv = (double)g32;
+    const double xn = (double)X[i] - gv;
+    X[i] = (float)xn;
+    const double dcv = (xn - gv) * inv_r;
+    const double cn = cdr[i] + dcv;
+    cdr[i] = cn;
+    send[t] = cn;  // the pencils take the new drift as it is: no update pass there
+    acc += 2.0 * dcv * gv + rd * dcv * dcv;  // the LAST role's norm term
+  }
+  __shared__ double sh[32];
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) parts[blockIdx.x] = t;
+}
+
+int pcb_apply_g_exchange(pcb_solver* h, uintptr_t recv_dev, uintptr_t send_dev, int P, int dz,
+                         int cp) {
+  if (!h || !recv_dev || !send_dev) return fail(PCB_E_ARG, "null argument");
+  if (h->precision != PCB_F32) return fail(PCB_E_ARG, "apply_g needs the f32 path");
+  if (h->n_own >= 0 && h->n_own != h->n) return fail(PCB_E_ARG, "halo slabs use pcb_apply_g");
+  if (P < 1 || dz < 1 || cp < 1 || (int64_t)P * cp * dz != h->n)
+    return fail(PCB_E_ARG, "exchange layout does not match the handle");
+  if (int e = set_dev(h)) return e;
+  const int g = grid_for(h->n, 256, NODE_GRID);
+  k_apply_g_xchg<<<g, 256, 0, h->stream>>>(h->G32.p, reinterpret_cast<const float*>(recv_dev),
+                                           reinterpret_cast<double*>(send_dev), h->X32.p,
+                                           h->cdrift.p, (int)h->n, P * cp, dz, cp,
+                                           1.0 / (double)h->r, (double)h->r, h->parts.p);
   LAUNCH_CHECK(h);
   k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p + 1, 0);
   LAUNCH_CHECK(h);

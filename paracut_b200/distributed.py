@@ -127,6 +127,26 @@ class SlabGeometry:
         assert rows.shape == (h, W - 1) and cols.shape == (h - 1, W)
         return GridEnergy((h, W), self.conn, w, [rows, cols, d1, d2])
 
+    def parts(self, rank):
+        """(slab, pencil) of rank as boxes of the global grid for the device
+        generator -- (origin, extent, handle dims, direction mask) each -- or
+        None where the layout is not a box (2D-8 halo slabs; a pencil that is
+        not whole rows of the plane)."""
+        if self.conn in HALO:
+            return None
+        D0, rest = self.dims[0], self.dims[1:]
+        k = CROSS[self.conn]
+        slab = ((rank * self.dz,) + (0,) * len(rest), (self.dz,) + rest, (self.dz,) + rest, 0xF)
+        if self.conn == "3D-6":
+            D1, D2 = rest
+            if self.cp % D2:
+                return None
+            rows = self.cp // D2
+            pencil = ((0, rank * rows, 0), (D0, rows, D2), (D0, 1, self.cp), 1 << k)
+        else:
+            pencil = ((0, rank * self.cp), (D0, self.cp), (D0, self.cp), 1 << k)
+        return slab, pencil
+
     def pencil_cols(self, rank):
         return np.arange(rank * self.cp, (rank + 1) * self.cp)
 
@@ -251,7 +271,7 @@ class ShardedAAR:
         import torch
         from . import _native as N
         self.N = N
-        g = as_grid(g)
+        g = as_grid(g)  # (a DeviceGrid passes through: ranks generate their parts)
         self.g = g
         self.comm = comm
         self.ranks = list(ranks)
@@ -260,9 +280,16 @@ class ShardedAAR:
         self.cross = CROSS[g.connectivity]
         self.slab, self.pencil = [], []
         self.halo = g.connectivity in HALO
+        dev = getattr(g, "_is_device_grid", False)
         for rk in self.ranks:
-            s = backend(self.geo.slab_grid(g, rk))
-            p = backend(self.geo.pencil_grid(g, rk))
+            parts = self.geo.parts(rk) if dev else None
+            if parts is not None:  # only the rank's slab and pencil, generated on its device
+                (so, se, sd, sm), (po, pe, pd, pm) = parts
+                s = backend(g.part(so, se, sd, sm))
+                p = backend(g.part(po, pe, pd, pm))
+            else:
+                s = backend(self.geo.slab_grid(g, rk))
+                p = backend(self.geo.pencil_grid(g, rk))
             s.set_family_mask(sum(1 << j for j in LOCAL[g.connectivity]))
             p.set_family_mask(1 << self.cross)
             if self.geo.halo(rk):
@@ -279,6 +306,7 @@ class ShardedAAR:
         for s, p in zip(self.slab, self.pencil):
             self._bufs.append(dict(Gs=self._tensor(s, N.BUF_G, np.float32),
                                    Gp=self._tensor(p, N.BUF_G, np.float32),
+                                   Cp=self._tensor(p, N.BUF_C, np.float64),
                                    Ns=self._tensor(s, N.BUF_NORMS, np.float64),
                                    Np=self._tensor(p, N.BUF_NORMS, np.float64)))
         P, dz, cp = self.geo.P, self.geo.dz, self.geo.cp
@@ -287,6 +315,9 @@ class ShardedAAR:
         if self.overlap:  # packed g (slab -> pencil), separate from G_s so S can run ahead
             self._send_g = [torch.empty((P, dz, cp), dtype=torch.float32, device=self._dev())
                             for _ in self.ranks]
+            # no halo: the slab sends the pencils their new drift (fp64) instead
+            self._send_c = ([torch.empty((P, dz, cp), dtype=torch.float64, device=self._dev())
+                             for _ in self.ranks] if not self.halo else None)
             self._streams = None
         if self.halo:
             self._hrow = [torch.empty(W, dtype=torch.float32, device=self._dev())
@@ -484,32 +515,47 @@ class ShardedAAR:
                                 b["Gs"][:W] += self._hrow[i]
                     if cuda:
                         S.wait_event(ev_a)
-                    for i, b in enumerate(self._bufs):
-                        b["Gs"][:ns].view(dz, P, cp).add_(self._recv_s[i].transpose(0, 1))
-                        self._send_g[i].copy_(b["Gs"][:ns].view(dz, P, cp).transpose(0, 1))
-                    if self.halo:  # the owner's complete first-row g -> the halo row
+                    if not self.halo:
+                        # one fused pass: g = G + d_z into the send buffer, and the update
+                        for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
+                            if hasattr(s, "host_buffer"):
+                                s.apply_g_exchange_host(self._recv_s[i].numpy(),
+                                                        self._send_c[i].numpy(), P, dz, cp)
+                            else:
+                                s.apply_g_exchange(self._recv_s[i].data_ptr(),
+                                                   self._send_c[i].data_ptr(), P, dz, cp)
+                            acc[i][k] += b["Ns"][1]
+                    else:
+                        for i, b in enumerate(self._bufs):
+                            b["Gs"][:ns].view(dz, P, cp).add_(self._recv_s[i].transpose(0, 1))
+                            self._send_g[i].copy_(b["Gs"][:ns].view(dz, P, cp).transpose(0, 1))
+                        # the owner's complete first-row g -> the halo row
                         self.comm.send_prev(
                             [b["Gs"][:W] if f else None for b, f in zip(self._bufs, first)],
                             [b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)])
-                    for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
-                        if hasattr(s, "host_buffer"):
-                            s.apply_g_host(b["Gs"].numpy())
-                        else:
-                            s.apply_g(b["Gs"].data_ptr())
-                        acc[i][k] += b["Ns"][1]
+                        for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
+                            if hasattr(s, "host_buffer"):
+                                s.apply_g_host(b["Gs"].numpy())
+                            else:
+                                s.apply_g(b["Gs"].data_ptr())
+                            acc[i][k] += b["Ns"][1]
                     ev_j = torch.cuda.Event() if cuda else None
                     if cuda:
                         ev_j.record(S)
-                with on(C):  # slab -> pencil g, pencil update (under the next slab sweeps)
+                with on(C):  # slab -> pencil (under the next slab sweeps)
                     if cuda:
                         C.wait_event(ev_j)
-                    recvs = [b["Gp"].view(P, dz, cp) for b in self._bufs]
-                    self.comm.all_to_all(self._send_g, recvs)
-                    for i, p in enumerate(self.pencil):
-                        if hasattr(p, "host_buffer"):
-                            p.apply_g_host(self._bufs[i]["Gp"].numpy())
-                        else:
-                            p.apply_g(self._bufs[i]["Gp"].data_ptr())
+                    if not self.halo:  # the new drift straight into the pencils' c
+                        self.comm.all_to_all(self._send_c,
+                                             [b["Cp"].view(P, dz, cp) for b in self._bufs])
+                    else:  # g, then the pencil update
+                        recvs = [b["Gp"].view(P, dz, cp) for b in self._bufs]
+                        self.comm.all_to_all(self._send_g, recvs)
+                        for i, p in enumerate(self.pencil):
+                            if hasattr(p, "host_buffer"):
+                                p.apply_g_host(self._bufs[i]["Gp"].numpy())
+                            else:
+                                p.apply_g(self._bufs[i]["Gp"].data_ptr())
         finally:
             if cuda:
                 base.wait_stream(S)

@@ -171,7 +171,13 @@ def inverse_normal(u):
 
 def noise(seed, start, count):
     """N(0, 1) values of nodes [start, start + count) for `seed`."""
-    i = np.arange(start, start + count, dtype=np.uint64)
+    return noise_at(seed, np.arange(start, start + count, dtype=np.uint64))
+
+
+def noise_at(seed, i):
+    """N(0, 1) values of the global node indices i (uint64 array) for `seed`."""
+    i = np.asarray(i, dtype=np.uint64)
+    count = i.size
     k0, k1 = int(seed) & 0xFFFFFFFF, (int(seed) >> 32) & 0xFFFFFFFF
     o0, o1, _, _ = _philox(i & _U32, i >> np.uint64(32),
                            np.full(count, NOISE_STREAM, np.uint64), np.zeros(count, np.uint64),
@@ -229,6 +235,58 @@ def _chunked(n, fn, chunk=1 << 21):
         return
     with ThreadPoolExecutor(max_workers=min(len(starts), os.cpu_count() or 1)) as ex:
         list(ex.map(lambda s0: fn(s0, min(chunk, n - s0)), starts))
+
+
+def make_part(spec, seed, gdims, origin, extent, dims, dir_mask=0xF, lam=None):
+    """Host reference of pcb_create_synthetic_box: the box [origin, origin +
+    extent) of the global instance (gdims), as a GridEnergy of `dims` (the
+    box's nodes in C order), with the box's internal edges of the directions
+    in dir_mask and zero weights elsewhere.  Equals slicing make_instance."""
+    if isinstance(spec, str):
+        spec = CONFIGS[spec]
+    gdims = tuple(int(d) for d in gdims)
+    nd = len(gdims)
+    centres, radii = shapes_of(gdims, spec.shapes, spec.rmin, spec.rmax, seed)
+    ext = tuple(int(e) for e in extent)
+    org = tuple(int(o) for o in origin)
+    img = np.full(ext, 0.3, dtype=np.float64)
+    for c, rad in zip(centres, radii):
+        lo = [max(max(0, int(math.floor(c[a] - rad))), org[a]) for a in range(nd)]
+        hi = [min(min(gdims[a], int(math.ceil(c[a] + rad)) + 1), org[a] + ext[a])
+              for a in range(nd)]
+        if any(h <= l for l, h in zip(lo, hi)):
+            continue
+        axes = [np.arange(l, h, dtype=np.float64) - c[a] for a, (l, h) in enumerate(zip(lo, hi))]
+        d2 = np.zeros([h - l for l, h in zip(lo, hi)])
+        for a, ax in enumerate(axes):
+            shape = [1] * nd
+            shape[a] = ax.size
+            d2 = d2 + (ax * ax).reshape(shape)
+        box = tuple(slice(l - o, h - o) for l, h, o in zip(lo, hi, org))
+        sub = img[box]
+        sub[d2 <= rad * rad] = 0.7
+    flat = img.reshape(-1)
+
+    def add_noise(s0, cnt):  # box flat index -> global node index, per chunk
+        t = np.arange(s0, s0 + cnt, dtype=np.int64)
+        gi = np.zeros(cnt, dtype=np.uint64)
+        coords = []
+        for a in range(nd - 1, -1, -1):
+            coords.append(t % ext[a] + org[a])
+            t = t // ext[a]
+        for a, c in zip(range(nd), reversed(coords)):
+            gi = gi * np.uint64(gdims[a]) + c.astype(np.uint64)
+        flat[s0:s0 + cnt] += SIGMA_NOISE * noise_at(seed, gi)
+
+    _chunked(flat.size, add_noise)
+    full = energy_from_image(img, spec.connectivity, lam=spec.lam if lam is None else lam,
+                             integer=spec.integer)
+    dims = tuple(int(d) for d in dims)
+    dws = []
+    for k, (d, a) in enumerate(zip(DIRECTIONS[spec.connectivity], full.dir_weights)):
+        shape = tuple(s - abs(o) for s, o in zip(dims, d))
+        dws.append(a.reshape(shape) if (dir_mask >> k) & 1 else np.zeros(shape))
+    return GridEnergy(dims, spec.connectivity, full.w, dws)
 
 
 def energy_from_image(img, connectivity, lam=1.0, integer=False):
@@ -298,11 +356,16 @@ class DeviceGrid:
         self.n = int(np.prod(self.dims))
         self._grid = None
 
+    def part(self, origin, extent, dims, dir_mask=0xF):
+        """The box [origin, origin + extent) as a device grid of `dims`
+        (pcb_create_synthetic_box; a sharded rank's slab or pencil)."""
+        return DeviceGridPart(self, origin, extent, dims, dir_mask)
+
     def load(self):
         """The instance with host arrays (generated on the device, copied back)."""
         if self._grid is None:
             from ._native import GridSolver
-            S = GridSolver(self, precision="f64", device=self.device)
+            S = GridSolver(self, precision="f32", device=self.device)  # (no fp64 hull spill)
             w, dws = S.get_instance(self.connectivity)
             S.close()
             self._grid = GridEnergy(self.dims, self.connectivity, w, dws)
@@ -335,3 +398,29 @@ class DeviceGrid:
     def _fingerprint(self):
         from .graph import instance_fingerprint
         return instance_fingerprint(self.load())
+
+
+class DeviceGridPart(DeviceGrid):
+    """A box of a DeviceGrid's global instance, generated on the device
+    (equals make_part / slicing make_instance)."""
+
+    def __init__(self, parent, origin, extent, dims, dir_mask=0xF):
+        self.spec, self.seed = parent.spec, parent.seed
+        self.connectivity, self.lam, self.integer = parent.connectivity, parent.lam, parent.integer
+        self.device = parent.device
+        self.centres, self.radii = parent.centres, parent.radii
+        self.dims = tuple(int(d) for d in dims)
+        self.n = int(np.prod(self.dims))
+        self.box = (tuple(parent.dims), tuple(int(o) for o in origin),
+                    tuple(int(e) for e in extent), int(dir_mask))
+        self._grid = None
+
+
+class HostPartsGrid(DeviceGrid):
+    """Like DeviceGrid for a sharded run, but each rank's slab and pencil are
+    generated on the host (make_part) and uploaded: the rank holds host arrays
+    of its own part only, never of the whole instance."""
+
+    def part(self, origin, extent, dims, dir_mask=0xF):
+        return make_part(self.spec, self.seed, self.dims, origin, extent, dims, dir_mask,
+                         lam=self.lam)

@@ -125,6 +125,13 @@ class EmuSolver:
         o = self.n_own
         self.norms[1] = float(np.sum(2.0 * dcv[:o] * gd[:o] + self.r * dcv[:o] * dcv[:o]))
 
+    def apply_g_exchange_host(self, recv, send, P, dz, cp):
+        """pcb_apply_g_exchange: g = G + d_z (fp32), apply_g, new drift into send [P][dz][cp]."""
+        g = (self.G.reshape(dz, P, cp) + np.asarray(recv, dtype=np.float32).reshape(P, dz, cp)
+             .transpose(1, 0, 2)).astype(np.float32)
+        self.apply_g_host(g.reshape(-1))
+        send.reshape(P, dz, cp)[...] = self.c.reshape(dz, P, cp).transpose(1, 0, 2)
+
     def shadow(self, want_y=True, want_s=False):
         for j in range(self.r):
             if (self.mask >> j) & 1:

@@ -167,3 +167,21 @@ def test_bench_helpers():
     assert cb["value"] > 0 and cb["cores"] >= 1 and cb["one_core"]["cores"] == 1
     assert "8x16x16" in cb["sample"] and cb["time_to_cut"]["extrapolated"]
     assert cb["time_to_cut"]["value"] == pytest.approx(cb["s_per_iter"] * 100)
+
+
+def test_rank_parts_equal_the_sliced_instance():
+    """A sharded rank's slab and pencil from the box generator (make_part, the
+    host reference of pcb_create_synthetic_box) equal the slices of the whole
+    instance that SlabGeometry takes."""
+    from paracut_b200.distributed import SlabGeometry
+    from paracut_b200.instances import make_part
+    for name, dims, P in (("cfg4", (8, 12, 16), 4), ("cfg2", (16, 24), 4), ("cfg5_int", (4, 8, 8), 2)):
+        g = make_instance(name, seed=3, dims=dims)
+        geo = SlabGeometry(dims, CONFIGS[name].connectivity, P)
+        for rk in range(P):
+            for desc, ref in zip(geo.parts(rk), (geo.slab_grid(g, rk), geo.pencil_grid(g, rk))):
+                o, e, d, m = desc
+                part = make_part(name, 3, dims, o, e, d, m)
+                assert part.dims == ref.dims and np.array_equal(part.w, ref.w)
+                for x, y in zip(part.dir_weights, ref.dir_weights):
+                    assert x.shape == y.shape and np.array_equal(x, y)
