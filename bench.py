@@ -508,7 +508,7 @@ def time_to_cut(pc, g, precision, device, reps=3):
     cfg = pc.SolverConfig(max_iters=20000, check_every=10, precision=precision, device=device,
                           thresholds=(0.0, 1e-6, -1e-6, 1e-3),
                           polish_iters=5000 if precision == "f32" else 0,
-                          polish_stall=40 if precision == "f32" else 0)
+                          polish_stall=10 if precision == "f32" else 0)
     walls, res = [], None
     for _ in range(reps):
         res = None

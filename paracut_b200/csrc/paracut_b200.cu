@@ -818,6 +818,34 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
       const int64_t lenL = L - (oL < 0 ? -oL : oL), loL = oL >= 0 ? 0 : -oL;
       const double* av = dw.p[k] + erow * lenL - loL;  // element (erow, x - loL)
       const uint8_t* bn = bits + base + joff;
+      if ((L & 3) == 0) {
+        // four positions per lane: the row's labels and the neighbours' as
+        // aligned 32-bit words (the neighbour row funnel-shifted into place);
+        // the weight is read only where a label differs (boundary edges)
+        const uint32_t* w32 = reinterpret_cast<const uint32_t*>(bits);
+        const int64_t nb0 = base + joff;  // neighbour of position 0
+        const unsigned sh = (unsigned)(nb0 & 3) * 8u;
+        for (int64_t x4 = (int64_t)lane * 4; x4 < L; x4 += 128) {
+          const uint32_t own = w32[(base + x4) >> 2];
+          const int64_t q = (nb0 + x4) >> 2;
+          const uint32_t lo = w32[q];
+          const uint32_t nb = sh ? __funnelshift_r(lo, w32[q + 1], sh) : lo;
+          const uint32_t diff4 = own ^ nb;
+          if (!diff4) continue;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int64_t x = x4 + b;
+            const unsigned diff = (diff4 >> (8 * b)) & 0xffu;
+            if (diff && x >= loL && x < loL + lenL) {
+              const double a = av[x];
+#pragma unroll
+              for (int t = 0; t < MAXT; ++t)
+                if ((diff >> t) & 1u) cut[t] += a;  // bits >= T are never set
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll 4
       for (int64_t x = loL + lane; x < loL + lenL; x += 32) {
         const unsigned diff = (unsigned)bits[base + x] ^ (unsigned)bn[x];
@@ -1062,6 +1090,7 @@ struct pcb_solver {
   bool y_valid = false;  // y holds the last shadow (not clobbered by aar_run)
   bool have_check = false;
   bool have_best = false;
+  bool x_in_best = false;  // the current check's x lives in bestx (pcb_keep_best swapped)
   int alg = 0;            // 0: AAR state; PCB_ALG_*: a dual scheme owns y/z
   double fista_t = 1.0;   // FISTA momentum parameter t_k
   int check_T = 0;
@@ -2302,7 +2331,9 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   }
   if (precision == PCB_F64)  // hull spill for the exact kernels (f32 path: lazily, project_K only)
     if ((rc = ensure_spill(h))) return bail(rc);
-  if ((rc = h->bits.alloc(n))) return bail(rc);
+  if ((rc = h->bits.alloc(n + 8))) return bail(rc);  // (+8: the cut kernel's word reads)
+  e = cudaMemset(h->bits.p, 0, n + 8);
+  if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "memset: %s", cudaGetErrorString(e)));
   if ((rc = h->xcur.alloc(n))) return bail(rc);
   if ((rc = h->parts.alloc(parts_needed(h)))) return bail(rc);
   if ((rc = h->vals.alloc(64))) return bail(rc);
@@ -2840,6 +2871,7 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
   CUDA_TRY(hostio::h2d(h->vals.p + 48, thr, nthr * sizeof(double), h->stream));
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   const int nv = nthr + 3;
+  h->x_in_best = false;  // (writes xcur afresh)
   k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n,
                                                  h->n_own < 0 ? h->n : h->n_own, nthr,
                                                  h->vals.p + 48,
@@ -2891,7 +2923,8 @@ int pcb_get_check(pcb_solver* h, int t, uint8_t* labels, int packed, double* x) 
     }
   }
   if (x)
-    CUDA_TRY(hostio::d2h(x, h->xcur.p, h->n * sizeof(double), h->stream));
+    CUDA_TRY(hostio::d2h(x, (h->x_in_best ? h->bestx : h->xcur).p, h->n * sizeof(double),
+                         h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -2982,8 +3015,12 @@ int pcb_keep_best(pcb_solver* h, int t) {
   k_labels<<<grid_for(h->n, 256, NODE_GRID), 256, 0, h->stream>>>(h->bits.p, h->n, t,
                                                                   h->bestlab.p);
   LAUNCH_CHECK(h);
-  CUDA_TRY(cudaMemcpyAsync(h->bestx.p, h->xcur.p, h->n * sizeof(double), cudaMemcpyDeviceToDevice,
-                           h->stream));
+  // the check's x becomes the best one by a buffer swap (the next check
+  // rewrites xcur); until then the current x is read from bestx
+  if (!h->x_in_best) {
+    swap_buf(h->xcur, h->bestx);
+    h->x_in_best = true;
+  }
   h->have_best = true;
   return 0;
 }
@@ -3075,7 +3112,7 @@ int pcb_level_set(pcb_solver* h, const double* x, double* u, double* energy) {
   DBuf<int64_t> last_of;
   DBuf<L::ArgMin> parts;
   DBuf<unsigned char> tmp;
-  const double* xd = h->xcur.p;
+  const double* xd = (h->x_in_best ? h->bestx : h->xcur).p;
   if (x) {
     if (int e = xin.alloc(n)) return e;
     CUDA_TRY(hostio::h2d(xin.p, x, n * sizeof(double), st));

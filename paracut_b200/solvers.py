@@ -66,6 +66,8 @@ class SolverConfig:
     polish_iters: int = 0   # f32 runs that end uncertified: up to this many f64 iterations
     polish_stall: int = 0   # f32: start the polish early once the best gap has not halved
                             # over this many checks (0: only at max_iters)
+    polish_precision: str = "f64s"  # the polish's fp64 mode: "f64s" (fast split
+                                    # kernels) or "f64" (bitwise reference kernels)
     level_sets: bool = False  # each check also tries the best level set of x (on the device)
 
     def __post_init__(self):
@@ -77,6 +79,8 @@ class SolverConfig:
             raise ValueError("tolerances must be >= 0")
         if self.threads < 1 or self.check_every < 1:
             raise ValueError("threads and check_every must be >= 1")
+        if self.polish_precision not in ("f64", "f64s"):
+            raise ValueError("polish_precision must be 'f64' or 'f64s'")
         if self.precision not in PRECISIONS:
             raise ValueError("precision must be one of %r" % (PRECISIONS,))
         if self.polish_iters < 0 or self.polish_stall < 0:
@@ -380,9 +384,10 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
     drv.stall = 0
     if polish and not drv.stopped:
         # fp32 state leaves a ~1e-5 floor on the discrete gap of large instances;
-        # continue in the exact fp64 mode from the same AAR point to certify
+        # continue in fp64 (the split fast kernels by default) from the same
+        # AAR point to certify
         S64 = (_make64() if _make64 is not None else
-               _native.GridSolver(g, precision="f64", device=cfg.device))
+               _native.GridSolver(g, precision=cfg.polish_precision, device=cfg.device))
         S64.set_z(S.get_z())
         drv.switch_solver(S64)
         drv.kmax = k + cfg.polish_iters
@@ -478,7 +483,7 @@ def solve_path(g, lambdas, cfg, keep_states=True):
         c = cfg if i == 0 else dataclasses.replace(cfg, warm_start=None, force_warm=True)
 
         def make64(lam=lam):
-            T = _native.GridSolver(g, precision="f64", device=cfg.device)
+            T = _native.GridSolver(g, precision=cfg.polish_precision, device=cfg.device)
             T.scale_pairwise(lam)
             return T
         res = solve_aar(gl, GridDecomposition(gl), c, _solver=S, _resident=i > 0,
