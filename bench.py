@@ -504,7 +504,7 @@ def time_to_cut(pc, g, precision, device, reps=3):
     """Second half of the metric: wall time to a certified optimal cut (gap <=
     1e-6, the reference's GAP_SLACK) through the public API from host arrays,
     reference stopping rule (checks every 10 iterations); f32 runs hand over to
-    the exact fp64 mode once the fp32 gap stalls.  Median of `reps` solves."""
+    the fast fp64 mode (f64s) once the fp32 gap stalls.  Median of `reps` solves."""
     cfg = pc.SolverConfig(max_iters=20000, check_every=10, precision=precision, device=device,
                           thresholds=(0.0, 1e-6, -1e-6, 1e-3),
                           polish_iters=5000 if precision == "f32" else 0,
