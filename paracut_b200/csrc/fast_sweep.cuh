@@ -580,6 +580,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   // have start = stop = 0); it is never active again, and its whole range
   // counts as emitted
   int i0 = start, k = start, c0x = -1, f0x = -1;
+  // weights of the edges left of the ceiling / floor points (a(c0x - 1),
+  // a(f0x - 1)): a bend's restart value without a ring read
+  R acx = R(0), afx = R(0);
   int ixi0 = rx(lane, start);  // ring index of the anchor i0
   double t = 0.0;          // z at the anchor: scan values are z - t
   R skr = R(0);            // running sum of (z - t) minus the anchor value
@@ -777,17 +780,20 @@ __global__ void __launch_bounds__(WARPS * 32)
         } else {
           const ST pold = rp[ix];
           const ST p32 = (ST)pn;
-          const double d = (double)p32 - (double)pold;
+          // d in the state type (fp32: one FADD, d rounded once; the G sums
+          // below are single fp32 adds, which equal the fp64-then-round form)
+          const ST dS = p32 - pold;
+          const double d = (double)dS;
           nq = nrm_d(d, nq);
           A.po[(pos * C32 + c32)] = p32;
           if (!ROWLIKE) {
             const int nd = node(base32, pos);
             if (ROLE == FIRST) {
-              A.G[nd] = (ST)d;
+              A.G[nd] = dS;
             } else if (ROLE == MID) {
-              A.G[nd] = (ST)((double)gpre[q] + d);
+              A.G[nd] = gpre[q] + dS;
             } else {
-              const ST g32 = (ST)((double)gpre[q] + d);
+              const ST g32 = gpre[q] + dS;
               const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
               A.Xo[nd] = (ST)xn;
@@ -797,7 +803,7 @@ __global__ void __launch_bounds__(WARPS * 32)
               nq = nrm_last(dcv, g, A.rd, nq);
             }
           } else {
-            ra[ix] = (ST)d;
+            ra[ix] = dS;
           }
         }
       }
@@ -833,9 +839,9 @@ __global__ void __launch_bounds__(WARPS * 32)
           } else if (ROLE == FIRST) {
             A.G[nd] = ra[ix];
           } else if (ROLE == MID) {
-            A.G[nd] = (ST)((double)gpre[ib] + (double)ra[ix]);
+            A.G[nd] = gpre[ib] + ra[ix];
           } else {
-            const ST g32 = (ST)((double)gpre[ib] + (double)ra[ix]);
+            const ST g32 = gpre[ib] + ra[ix];
             const double g = (double)g32;
             const double xn = (double)xpre[ib] - g;
             A.Xo[nd] = (ST)xn;
@@ -895,6 +901,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const R u = sE + rk;
         const bool cu = u <= Lc;
         c0x = cu ? k : c0x;
+        acx = cu ? rk : acx;
         cs = cu ? u * inv : cs;
         Lc = cu ? u : Lc;
         const bool b1 = cs < fs;  // ceiling dips under the floor cone
@@ -902,6 +909,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const R l = sE - rk;
         const bool fu = !b1 && l >= Lf;
         f0x = fu ? k : f0x;
+        afx = fu ? rk : afx;
         fs = fu ? l * inv : fs;
         Lf = fu ? l : Lf;
         const bool b2 = !b1 && fs > cs;       // floor rises over the ceiling cone
@@ -919,12 +927,10 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int bk = tf ? f0x : (tc ? c0x : k);
         const R fill = tf ? fs : (tc ? cs : sE * inv);
         // ---- close segment [i0, bk): its prox value is the string slope `fill` (+ t)
-        R ab = (R)ra[rx(lane, bk - 1)];
         int s0 = i0;
         R qv = -fill;  // q = z_i0 - fill, and z_i0 - t = 0
         if (LAG && bend && i0 < lo_pos) {
           const double fabs_ = (double)fill + t;
-          if (bk - 1 < lo_pos) ab = (R)a_global(A, ((bk - 1) * C32 + c32));
           const int e2 = min(min(bk, lo_pos), stop);
           for (int j = i0; j < e2; ++j)
             nrm += finish_global<ROLE, ST>(A, (j * C32 + c32), node(base32, j), fabs_);
@@ -944,8 +950,9 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
         smask |= (unsigned)mark << (s0 & (RL - 1));
         // after a touch the string leaves the tube point: skr = -touch * a(bk-1)
-        // (a free piece end restarts at 0)
-        const R nskr = tf ? ab : (tc ? -ab : R(0));
+        // (a free piece end restarts at 0; a touch at the unit's stop gate, where
+        // rk = 0 was recorded, ends the unit)
+        const R nskr = tf ? afx : (tc ? -acx : R(0));
         i0 = bend ? bk : i0;
         k = bend ? bk : k;
         skr = bend ? nskr : skr;
@@ -972,6 +979,8 @@ __global__ void __launch_bounds__(WARPS * 32)
             const R rk1 = (R)an;
             c0x = k1;
             f0x = k1;
+            acx = rk1;
+            afx = rk1;
             cs = skr + rk1;
             Lc = cs;
             fs = skr - rk1;

@@ -68,6 +68,9 @@ class SolverConfig:
                             # over this many checks (0: only at max_iters)
     polish_precision: str = "f64s"  # the polish's fp64 mode: "f64s" (fast split
                                     # kernels) or "f64" (bitwise reference kernels)
+    polish_gap: float = 0.0  # f32 + polish_stall: stall only counts once the best gap is at
+                             # most this (0: any gap), so a plateau far above the fp32
+                             # noise floor keeps the cheaper f32 iterations going
     level_sets: bool = False  # each check also tries the best level set of x (on the device)
 
     def __post_init__(self):
@@ -83,8 +86,8 @@ class SolverConfig:
             raise ValueError("polish_precision must be 'f64' or 'f64s'")
         if self.precision not in PRECISIONS:
             raise ValueError("precision must be one of %r" % (PRECISIONS,))
-        if self.polish_iters < 0 or self.polish_stall < 0:
-            raise ValueError("polish_iters and polish_stall must be >= 0")
+        if self.polish_iters < 0 or self.polish_stall < 0 or self.polish_gap < 0:
+            raise ValueError("polish_iters, polish_stall and polish_gap must be >= 0")
         thr = tuple(float(t) for t in self.thresholds)
         if not 1 <= len(thr) <= MAX_THRESHOLDS:
             raise ValueError("1..%d thresholds supported" % MAX_THRESHOLDS)
@@ -293,6 +296,8 @@ class _Driver:
     def stalled(self):
         """The best gap has not halved over the last `stall` checks."""
         h, w = self._best_hist, self.stall
+        if w > 0 and self.cfg.polish_gap > 0 and not h[-1] <= self.cfg.polish_gap:
+            return False
         return w > 0 and len(h) > w and not h[-1] <= 0.5 * h[-1 - w]
 
     def due(self, k):
