@@ -408,11 +408,13 @@ class GridSolver:
     def keep_best(self, t):
         check(lib().pcb_keep_best(self.handle, int(t)))
 
-    def get_best(self):
-        lab = _host_empty((self.n,), np.uint8)
-        x = _host_empty((self.n,))
-        check(lib().pcb_get_best(self.handle, ptr(lab), ptr(x)))
-        return lab, x
+    def get_best(self, labels=True, x=True):
+        """(labels uint8, x fp64) of the kept best iterate; either may be skipped (None)."""
+        lab = _host_empty((self.n,), np.uint8) if labels else None
+        xv = _host_empty((self.n,)) if x else None
+        check(lib().pcb_get_best(self.handle, ptr(lab) if labels else None,
+                                 ptr(xv) if x else None))
+        return lab, xv
 
     def scale_pairwise(self, factor):
         """Pairwise weights := factor * creation weights; AAR state kept."""

@@ -123,6 +123,25 @@ class SolveResult:
     threshold: float = 0.0   # primal threshold of the reported labeling (extension)
 
 
+class _DeviceSolveResult(SolveResult):
+    """SolveResult whose tv_solution (n fp64, the largest read-back) is copied
+    from the device on first access; the handle that kept the best iterate is
+    held until then.  Used only when that handle is private to the solve."""
+
+    @property
+    def tv_solution(self):
+        if self._x is None and self._xsrc is not None:
+            _, self._x = self._xsrc.get_best(labels=False, x=True)
+            self._xsrc = None
+        return self._x
+
+    @tv_solution.setter
+    def tv_solution(self, v):
+        self._x = v
+        if v is not None:
+            self._xsrc = None
+
+
 def threshold(x):
     """x_i > 0 -> 1, else 0 (strict; solvers.py:81-83)."""
     return (np.asarray(x) > 0).astype(np.uint8)
@@ -207,6 +226,7 @@ class _Driver:
         self.stopped = False
         self._labs = []
         self.thr = np.asarray(cfg.thresholds, dtype=np.float64)
+        self.owned = solver is None  # handles created here serve this solve only
         self.solver = (solver if solver is not None else
                        _native.GridSolver(g, precision=cfg.precision, device=cfg.device))
         self.best_solver = None
@@ -325,7 +345,9 @@ class _Driver:
 
     def finish(self, state=None):
         wall = time.perf_counter() - self.t0
-        lab, x = (self.best_solver or self.solver).get_best()
+        src = self.best_solver or self.solver
+        lazy_x = self.owned  # no later solve reuses the handle: x on first access
+        lab, x = src.get_best(labels=True, x=not lazy_x)
         certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
         if self.cfg.reference is None and self.log:
             self.flush_norms()
@@ -346,11 +368,15 @@ class _Driver:
             self.flush_norms()
         if state is None:
             state = _DeviceDualState(self.solver, self.g)
-        return SolveResult(labeling=lab, tv_solution=x, energy=self.best_energy,
-                           gap=self.best_gap, iterations=self.iterations, certified=certified,
-                           dual_state=state, trace=self.trace, wall_time=wall,
-                           algorithm=self.cfg.algorithm, monitor=self.monitor,
-                           threshold=self.best_thr)
+        cls = _DeviceSolveResult if lazy_x else SolveResult
+        res = cls(labeling=lab, tv_solution=x, energy=self.best_energy,
+                  gap=self.best_gap, iterations=self.iterations, certified=certified,
+                  dual_state=state, trace=self.trace, wall_time=wall,
+                  algorithm=self.cfg.algorithm, monitor=self.monitor,
+                  threshold=self.best_thr)
+        if lazy_x:
+            res._xsrc = src
+        return res
 
 
 def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):

@@ -6,11 +6,11 @@ sys.path.insert(0, '.')
 import numpy as np
 import paracut_b200 as pc
 from paracut_b200 import _native
-from paracut_b200.instances import make_instance
+from paracut_b200.instances import CONFIGS, make_instance
 
 wl = sys.argv[1] if len(sys.argv) > 1 else 'cfg4'
 K = int(sys.argv[2]) if len(sys.argv) > 2 else 200
-g = make_instance(wl, seed=0)
+g = make_instance(CONFIGS[wl], seed=0)
 for rep in range(3):
     t = [time.perf_counter()]
     S = _native.GridSolver(g, precision='f32'); S.synchronize(); t.append(time.perf_counter())
@@ -30,3 +30,11 @@ for rep in range(3):
     t1 = time.perf_counter()
     del res
     print("solve total %.1f ms" % ((t1 - t0) * 1e3))
+
+import cProfile, pstats
+pr = cProfile.Profile()
+pr.enable()
+res = pc.solve(g, pc.decompose_grid(g), pc.SolverConfig(max_iters=K, check_every=K + 1, precision='f32'))
+_ = res.labeling.sum()
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(25)
