@@ -488,6 +488,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   // device-side choice between the two sweeps of a family (both are launched;
   // the one the mode word does not select returns at once)
   if (A.vmode != nullptr && ((*A.vmode == 1) != VER)) return;
+  // the next (programmatically launched) sweep may start once every block of
+  // this one has started: it fills this grid's tail
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const Fam F = A.F;
@@ -703,9 +706,18 @@ __global__ void __launch_bounds__(WARPS * 32)
   };
 
   // G/X of tile T into registers (mode A natural; mode B rows for row-like MID)
+  bool dep_ok = false;  // the previous sweep's output (G, X) may be read
   auto prefetch = [&](int T) {
     pre_tile = T;
     if (ROLE != MID && ROLE != LAST) return;
+    if (!dep_ok) {
+      // programmatic dependent launch: everything before this point reads
+      // only this family's state, its weights and the drift; G / X (and the
+      // LAST role's writes of X and c) come after the previous grid is done.
+      // A no-op when the kernel was launched the ordinary way.
+      asm volatile("griddepcontrol.wait;\n" ::: "memory");
+      dep_ok = true;
+    }
     const int k0 = T * TP;
     if (!ROWLIKE) {
 #pragma unroll
@@ -1109,7 +1121,9 @@ __global__ void __launch_bounds__(WARPS * 32)
     for (;;) {
       const int lo_pos = t_lo * TP;
       const int avail_hi = min(t_rdy * TP, m);
-      if (pre_tile != t_lo) prefetch(t_lo);
+      // (MID / LAST: not before the first retire, so that a programmatic
+      // launch scans its first tiles while the previous sweep drains)
+      if (pre_tile != t_lo && (dep_ok || (ROLE != MID && ROLE != LAST))) prefetch(t_lo);
       // ---------------- scan until every lane needs data beyond avail_hi.
       // One gate per trip.  Warps with no lagging lane (the normal case) run
       // a variant without any below-the-ring checks, with the segment close

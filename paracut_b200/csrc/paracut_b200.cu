@@ -1160,6 +1160,11 @@ struct pcb_solver {
   // merges of a step run on a side stream, overlapping the sweeps (they
   // depend only on the state at the start of the step)
   bool overlap_merges = true;  // PCB_OVERLAP_MERGE=0 runs them inline
+  // programmatic dependent launch of the MID / LAST sweeps of a plain step
+  // (PCB_PDL=0: off): their scans start in the previous sweep's tail, the
+  // first read of its output waits in griddepcontrol.wait
+  bool use_pdl = true;
+  bool pdl_launch = false;  // the next launch_sweep is programmatic
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_merge[MAXR] = {};
   // profiling: event pairs around family launches
@@ -1569,7 +1574,21 @@ int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fas
   }
   const int per = pcb::fast::WARPS * 32;
   const dim3 g((unsigned)((a.F.C + per - 1) / per), (unsigned)(a.merge ? a.nb : 1));
-  pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST><<<g, per, bytes, h->stream>>>(a, M);
+  if (h->pdl_launch) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g;
+    cfg.blockDim = dim3(per);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST>, a, M));
+  } else {
+    pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST><<<g, per, bytes, h->stream>>>(a, M);
+  }
   LAUNCH_CHECK(h);
   return 0;
 }
@@ -1901,11 +1920,18 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     }
     prof_begin(h, j);
     if (!side_merge[j]) rc = launch_merge(h, j, a);
+    // MID / LAST of a plain single-buffer step: programmatic launch (their
+    // scans read only p_j, the weights and the drift, none of which the
+    // previous sweep writes; k_sweep waits before reading G / X).  Not when
+    // per-family events are recorded in between or a merge ran inline.
+    h->pdl_launch = h->use_pdl && flags == 0 && !dbuf && role != pcb::fast::FIRST &&
+                    !h->profiling && (side_merge[j] || h->nbk[j] <= 1);
     if (!rc) {
       if (role == pcb::fast::FIRST) rc = launch_role_v<pcb::fast::FIRST, ST>(h, a, j);
       else if (role == pcb::fast::MID) rc = launch_role_v<pcb::fast::MID, ST>(h, a, j);
       else rc = launch_role_v<pcb::fast::LAST, ST>(h, a, j);
     }
+    h->pdl_launch = false;
     prof_end(h);
     if (rc) return rc;
     off += fam_units(h, j);
@@ -1990,6 +2016,8 @@ int choose_split(pcb_solver* h) {
     if (int e = h->merge.alloc(need)) return e;
   const char* ov = getenv("PCB_OVERLAP_MERGE");
   h->overlap_merges = !(ov && ov[0] == '0');
+  const char* pd = getenv("PCB_PDL");
+  h->use_pdl = !(pd && pd[0] == '0');
   return 0;
 }
 
