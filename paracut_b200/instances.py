@@ -422,5 +422,9 @@ class HostPartsGrid(DeviceGrid):
     of its own part only, never of the whole instance."""
 
     def part(self, origin, extent, dims, dir_mask=0xF):
-        return make_part(self.spec, self.seed, self.dims, origin, extent, dims, dir_mask,
-                         lam=self.lam)
+        key = (tuple(origin), tuple(extent), tuple(dims), int(dir_mask))
+        cache = self.__dict__.setdefault("_parts", {})
+        if key not in cache:  # built once: a rank's host-side input arrays
+            cache[key] = make_part(self.spec, self.seed, self.dims, origin, extent, dims,
+                                   dir_mask, lam=self.lam)
+        return cache[key]
