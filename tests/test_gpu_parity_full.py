@@ -9,6 +9,8 @@ printed so the GPU test log records them.
 
 * cfg2 2D-4 1024^2, 500 iterations: f64 and f32;
 * cfg4 3D-6 256^3, 500 iterations: f32 (the benchmarked path) and f64;
+* cfg2 and cfg4 in the fast fp64 mode (f64s: split chains, fp64 state and
+  scans -- the polish of a time-to-cut solve), 1e-6;
 * cfg3 2D-8 4096^2, 1000 iterations: f32;
 * cfg2_int 1024^2: the device certificate (pcb_check: labels, cut energy,
   gap, smooth dual at thresholds 0 and +-1e-6) of the oracle's own iterate
@@ -84,6 +86,16 @@ def test_cfg4_full_f32_and_f64(cfg4_ref, capsys):
     _report(capsys, "cfg4 256^3 k=500: f32 rel %.3e, f64 rel %.3e (bitwise %s)" % (e32, e64, bitwise))
     assert e32 <= 1e-4
     assert e64 <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg4"])
+def test_full_f64s(name, cfg2_ref, cfg4_ref, capsys):
+    g, _, y_ref = cfg2_ref if name == "cfg2" else cfg4_ref
+    x_ref = g.w - y_ref.sum(axis=0)
+    st = _device(g, 500, "f64s")
+    e = _rel(g.w - st.y.sum(axis=0), x_ref)
+    _report(capsys, "%s k=500: f64s rel %.3e" % (name, e))
+    assert e <= 1e-6
 
 
 def test_cfg3_full_f32(capsys):
