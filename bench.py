@@ -433,6 +433,7 @@ def main():
     mean_ms = fam_ms[fam] / max(int(fam_cnt[fam]), 1)
     achieved = per_launch / (mean_ms / 1e3) / 1e9
     traffic = _ncu_traffic(args.workload, fam)
+    issue = _ncu_issue(args.workload, fam, mean_ms)
     B_iter = algorithmic_bytes(g, r, b)
     roof = {"bound": "hbm", "achieved": achieved, "peak": pk, "unit": "GB/s",
             "frac": achieved / pk, "traffic": traffic,
@@ -443,7 +444,8 @@ def main():
             "peak_kind": pk_kind,
             "per_family_ms": [float(v / max(int(c), 1)) for v, c in zip(fam_ms, fam_cnt)],
             "iteration_achieved_gbs": B_iter * args.steps / (ms / 1e3) / 1e9,
-            "iteration_bytes": B_iter}
+            "iteration_bytes": B_iter, "iteration_frac": B_iter * args.steps / (ms / 1e3) / 1e9 / pk,
+            "issue": issue}
 
     e2e = None
     if not args.no_e2e:
@@ -560,6 +562,24 @@ def _family_edges(g):
     z0 = int(np.count_nonzero(d1[:, even])) + int(np.count_nonzero(d2[:, ~even]))
     z1 = int(np.count_nonzero(d2[:, even])) + int(np.count_nonzero(d1[:, ~even]))
     return [nz[0], nz[1], z0, z1]
+
+
+def _ncu_issue(workload, fam, mean_ms, sms=148, sm_ghz=1.965):
+    """The instruction-issue roofline of the same kernel: its warp instructions
+    per launch (committed ncu capture) / its live mean launch time, against 4
+    warp instructions per cycle per SM at the max SM clock."""
+    path = os.path.join(ROOT, "profiles", "ncu_issue.json")
+    try:
+        with open(path) as f:
+            inst = json.load(f).get(workload, {}).get(str(fam))
+    except Exception:
+        inst = None
+    if not inst or not mean_ms:
+        return None
+    achieved = inst / (mean_ms / 1e3) / 1e9
+    peak = sms * 4 * sm_ghz
+    return {"bound": "issue", "warp_instructions": inst, "achieved": achieved, "peak": peak,
+            "unit": "G warp-instr/s", "frac": achieved / peak}
 
 
 def _ncu_traffic(workload, fam):
