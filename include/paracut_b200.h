@@ -131,8 +131,6 @@ int pcb_aar_run(pcb_solver *h, int64_t iters, double *step_norms);
 #define PCB_STEP_NO_UPDATE 2  /* no LAST role: drift/primal updated elsewhere      */
 #define PCB_STEP_EXPORT_G 4   /* LAST stores its per-node g = sum_j d_j in G       */
 #define PCB_STEP_NORM_RAW 8   /* step_norms receive sums of squares (partials)    */
-#define PCB_STEP_XCHG 16      /* LAST adds the exchanged cross-family d and writes
-                                 the new drift to the send buffer (pcb_set_exchange) */
 int pcb_aar_step(pcb_solver *h, int64_t iters, int flags, double *step_norms);
 /* Sweep only families whose bit is set (decompose_grid order). */
 int pcb_set_family_mask(pcb_solver *h, unsigned mask);
@@ -149,14 +147,6 @@ int pcb_apply_g(pcb_solver *h, uintptr_t g_dev);
  * halo row (3D-6, 2D-4). */
 int pcb_apply_g_exchange(pcb_solver *h, uintptr_t recv_dev, uintptr_t send_dev, int P, int dz,
                          int cp);
-/* Register the exchange buffers of PCB_STEP_XCHG: recv = device
- * float[P][dz][cp] (the cross family's d from the pencils), send = device
- * double[P][dz][cp] (the new drift for the pencils).  The slab's LAST sweep
- * then does what pcb_apply_g_exchange does, inside its retire pass:
- * g = (G + d_last) + d_z, x -= g, c += (x - g)/r, c -> send (its norm term
- * in the step norm).  Slabs without a halo row (3D-6, 2D-4). */
-int pcb_set_exchange(pcb_solver *h, uintptr_t recv_dev, uintptr_t send_dev, int P, int dz,
-                     int cp);
 /* Nodes [n_own, n) of this handle are halo copies of nodes another shard
  * owns (2D-8 row slabs carry the next slab's first row for the zig-zag path
  * that straddles the boundary): pcb_check labels them (their edges to owned

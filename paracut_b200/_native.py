@@ -18,7 +18,6 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libparacut_b200.so")
 
 PCB_E_ARG, PCB_E_CUDA, PCB_E_STATE, PCB_E_NOMEM = -1, -2, -3, -4
 STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
-STEP_XCHG = 16
 BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_P, BUF_BITS = 0, 1, 2, 3, 4, 5, 6
 ALG_BCD, ALG_AP, ALG_FISTA = 1, 2, 3
 CONN_CODES = {"2D-4": 0, "2D-8": 1, "3D-6": 2}
@@ -77,7 +76,6 @@ def _declare(L):
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_verify_stats.argtypes = [P, P, P, P, P, P]
     L.pcb_apply_g_exchange.argtypes = [P, ctypes.c_size_t, ctypes.c_size_t, INT, INT, INT]
-    L.pcb_set_exchange.argtypes = [P, ctypes.c_size_t, ctypes.c_size_t, INT, INT, INT]
     L.pcb_create_synthetic.argtypes = [P, INT, INT, INT, P, P, ctypes.c_uint64, ctypes.c_double,
                                        INT, INT, INT, P]
     L.pcb_get_instance.argtypes = [P, P, P]
@@ -106,7 +104,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
            "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance",
-           "pcb_apply_g_exchange", "pcb_create_synthetic_box", "pcb_set_exchange")
+           "pcb_apply_g_exchange", "pcb_create_synthetic_box")
 
 
 def lib():
@@ -313,11 +311,6 @@ class GridSolver:
 
     def apply_g(self, g_dev_ptr):
         check(lib().pcb_apply_g(self.handle, int(g_dev_ptr)))
-
-    def set_exchange(self, recv_ptr, send_ptr, P, dz, cp):
-        """Buffers of STEP_XCHG steps (pcb_set_exchange)."""
-        check(lib().pcb_set_exchange(self.handle, int(recv_ptr), int(send_ptr), int(P),
-                                     int(dz), int(cp)))
 
     def apply_g_exchange(self, recv_ptr, send_ptr, P, dz, cp):
         """g = G + received d_z, into the send buffer and applied (pcb_apply_g_exchange)."""

@@ -97,26 +97,7 @@ struct ArgsT {
   uint16_t* sg;
   const int* vmode; // device mode word of this family: 1 = VER sweeps, else SCAN
   int* vcount;      // SCAN: chains whose hints changed; VER: chains repaired
-  // LAST role of a sharded slab (distributed.py): g also takes the cross
-  // family's d received in the pencil -> slab all-to-all (gz), and the new
-  // drift is also written into the slab -> pencil send buffer (csend); both in
-  // the exchange layout [P][dz][cp] (t = (q * dz + zr) * cp + cc for node
-  // zr * plane + q * cp + cc).  nullptr: no exchange.
-  const float* gz = nullptr;
-  double* csend = nullptr;
-  int xplane = 1, xdz = 1, xcp = 1;
-  int xsh_plane = -1, xsh_cp = -1;  // log2 of xplane / xcp when powers of two
 };
-
-// exchange-layout index of a slab node (ArgsT::gz / csend)
-template <class ST>
-__device__ __forceinline__ int xchg_index(const ArgsT<ST>& A, int nd) {
-  const int zr = A.xsh_plane >= 0 ? nd >> A.xsh_plane : nd / A.xplane;
-  const int col = nd - zr * A.xplane;
-  const int q = A.xsh_cp >= 0 ? col >> A.xsh_cp : col / A.xcp;
-  const int cc = col - q * A.xcp;
-  return (q * A.xdz + zr) * A.xcp + cc;
-}
 
 using Args = ArgsT<float>;
 using Args64 = ArgsT<double>;
@@ -286,18 +267,12 @@ __device__ __noinline__ double finish_global(const ArgsT<ST>& A, int64_t fi, int
   } else if (ROLE == MID) {
     A.G[nd] = (ST)((double)A.Gi[nd] + d);
   } else {
-    ST g32 = (ST)((double)A.Gi[nd] + d);
-    int t = 0;
-    if (A.gz) {
-      t = xchg_index(A, (int)nd);
-      g32 = g32 + A.gz[t];
-    }
+    const ST g32 = (ST)((double)A.Gi[nd] + d);
     const double g = (double)g32;
     const double xn = (double)A.X[nd] - g;
     A.Xo[nd] = (ST)xn;
     const double dcv = (xn - g) * A.inv_r;
     A.co[nd] = cz + dcv;
-    if (A.csend) A.csend[t] = cz + dcv;
     if (A.export_g) A.G[nd] = g32;
     nrm = nrm_last(dcv, g, A.rd, nrm);
   }
@@ -640,7 +615,6 @@ __global__ void __launch_bounds__(WARPS * 32)
 
   // retire-only inputs prefetched into registers (G for MID/LAST, X for LAST)
   ST gpre[TP], xpre[TP];
-  float gzpre[TP];  // LAST of a sharded slab: the exchanged cross-family d
   int pre_tile = -1;
 
   int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
@@ -684,8 +658,6 @@ __global__ void __launch_bounds__(WARPS * 32)
         if (warp_live && pos < m && (lane < 8 || (ROLE == LAST && lane < 16)))
           l2_prefetch((lane < 8 ? (const void*)(A.Gi + node(b0, pos))
                                 : (const void*)(A.X + node(b0, pos))));
-        if (ROLE == LAST && A.gz && warp_live && pos < m && lane >= 16 && lane < 24)
-          l2_prefetch(A.gz + xchg_index(A, node(b0, pos)));
       } else if (valid && k0 < m) {  // each lane: its chain's 8 positions
         l2_prefetch(A.Gi + node(base32, k0));
         if (ROLE == LAST) l2_prefetch(A.X + node(base32, k0));
@@ -755,7 +727,6 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int nd = pr ? node(base32, pos) : 0;
         gpre[q] = pr ? A.Gi[nd] : ST(0);
         if (ROLE == LAST) xpre[q] = pr ? A.X[nd] : ST(0);
-        if (ROLE == LAST && A.gz) gzpre[q] = pr ? A.gz[xchg_index(A, nd)] : 0.f;
       }
     } else {
       const int pos = k0 + (lane & 7);
@@ -767,7 +738,6 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int nd = pr ? node(bi, pos) : 0;
         gpre[ib] = pr ? A.Gi[nd] : ST(0);
         if (ROLE == LAST) xpre[ib] = pr ? A.X[nd] : ST(0);
-        if (ROLE == LAST && A.gz) gzpre[ib] = pr ? A.gz[xchg_index(A, nd)] : 0.f;
       }
     }
   };
@@ -835,15 +805,12 @@ __global__ void __launch_bounds__(WARPS * 32)
             } else if (ROLE == MID) {
               A.G[nd] = gpre[q] + dS;
             } else {
-              ST g32 = gpre[q] + dS;
-              if (A.gz) g32 = g32 + (ST)gzpre[q];  // sharded slab: + the cross family's d
+              const ST g32 = gpre[q] + dS;
               const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
               A.Xo[nd] = (ST)xn;
               const double dcv = (xn - g) * A.inv_r;
-              const double cn = (zj - (double)pold) + dcv;  // c_old = z - p_old
-              A.co[nd] = cn;
-              if (A.csend) A.csend[xchg_index(A, nd)] = cn;
+              A.co[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
               if (A.export_g) A.G[nd] = g32;
               nq = nrm_last(dcv, g, A.rd, nq);
             }
@@ -886,15 +853,12 @@ __global__ void __launch_bounds__(WARPS * 32)
           } else if (ROLE == MID) {
             A.G[nd] = gpre[ib] + ra[ix];
           } else {
-            ST g32 = gpre[ib] + ra[ix];
-            if (A.gz) g32 = g32 + (ST)gzpre[ib];
+            const ST g32 = gpre[ib] + ra[ix];
             const double g = (double)g32;
             const double xn = (double)xpre[ib] - g;
             A.Xo[nd] = (ST)xn;
             const double dcv = (xn - g) * A.inv_r;
-            const double cn = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
-            A.co[nd] = cn;
-            if (A.csend) A.csend[xchg_index(A, nd)] = cn;
+            A.co[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
             if (A.export_g) A.G[nd] = g32;
             double& nq = (ib & 1) ? nb : na;
             nq = nrm_last(dcv, g, A.rd, nq);

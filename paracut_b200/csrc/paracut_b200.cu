@@ -1165,10 +1165,6 @@ struct pcb_solver {
   // first read of its output waits in griddepcontrol.wait
   bool use_pdl = true;
   bool pdl_launch = false;  // the next launch_sweep is programmatic
-  // PCB_STEP_XCHG buffers (pcb_set_exchange)
-  const float* xg_recv = nullptr;
-  double* xg_send = nullptr;
-  int xg_P = 0, xg_dz = 0, xg_cp = 0;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_merge[MAXR] = {};
   // profiling: event pairs around family launches
@@ -1889,18 +1885,6 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     pcb::fast::ArgsT<ST> a{F, P + (int64_t)j * h->n, FastState<ST>::wf(h, j), h->cdrift.p, G,
                            X, nullptr, inv_r, rd, h->parts.p + off, nullptr, 1,
                            (flags & PCB_STEP_EXPORT_G) ? 1 : 0};
-    if constexpr (F32) {
-      if ((flags & PCB_STEP_XCHG) && role == pcb::fast::LAST) {
-        a.gz = h->xg_recv;
-        a.csend = h->xg_send;
-        a.xplane = h->xg_P * h->xg_cp;
-        a.xdz = h->xg_dz;
-        a.xcp = h->xg_cp;
-        auto lg2 = [](int v) { return (v > 0 && (v & (v - 1)) == 0) ? __builtin_ctz((unsigned)v) : -1; };
-        a.xsh_plane = lg2(a.xplane);
-        a.xsh_cp = lg2(a.xcp);
-      }
-    }
     if (dbuf) {
       a.po = (ST*)h->p32b.p + (int64_t)j * h->n;
       a.co = h->cdriftb.p;
@@ -2783,8 +2767,6 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   if (!h) return fail(PCB_E_ARG, "null handle");
   if (h->alg) return fail(PCB_E_STATE, "handle holds a dual-scheme state (init_cold/set_z for AAR)");
   if (flags && h->precision != PCB_F32) return fail(PCB_E_ARG, "step flags need the f32 path");
-  if ((flags & PCB_STEP_XCHG) && (!h->xg_recv || (flags & PCB_STEP_NO_UPDATE)))
-    return fail(PCB_E_ARG, "PCB_STEP_XCHG needs pcb_set_exchange and a LAST role");
   if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
   if (!h->have_state) return fail(PCB_E_STATE, "no AAR state (call init_cold or set_z)");
   if (iters == 0) return 0;
@@ -3311,21 +3293,6 @@ int pcb_apply_g_exchange(pcb_solver* h, uintptr_t recv_dev, uintptr_t send_dev, 
   LAUNCH_CHECK(h);
   k_reduce_norm<<<1, 1024, 0, h->stream>>>(h->parts.p, g, h->norms.p + 1, 0);
   LAUNCH_CHECK(h);
-  return 0;
-}
-
-int pcb_set_exchange(pcb_solver* h, uintptr_t recv_dev, uintptr_t send_dev, int P, int dz,
-                     int cp) {
-  if (!h || !recv_dev || !send_dev) return fail(PCB_E_ARG, "null argument");
-  if (h->precision != PCB_F32) return fail(PCB_E_ARG, "the exchange step needs the f32 path");
-  if (h->n_own >= 0 && h->n_own != h->n) return fail(PCB_E_ARG, "halo slabs use pcb_apply_g");
-  if (P < 1 || dz < 1 || cp < 1 || (int64_t)P * cp * dz != h->n)
-    return fail(PCB_E_ARG, "exchange layout does not match the handle");
-  h->xg_recv = reinterpret_cast<const float*>(recv_dev);
-  h->xg_send = reinterpret_cast<double*>(send_dev);
-  h->xg_P = P;
-  h->xg_dz = dz;
-  h->xg_cp = cp;
   return 0;
 }
 

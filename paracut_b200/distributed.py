@@ -267,7 +267,7 @@ class ShardedAAR:
     emulation in tests).
     """
 
-    def __init__(self, g, comm, ranks, backend, device=None, overlap=None, fused_last=None):
+    def __init__(self, g, comm, ranks, backend, device=None, overlap=None):
         import torch
         from . import _native as N
         self.N = N
@@ -302,9 +302,6 @@ class ShardedAAR:
         self.device = device
         # overlapped schedule (module docstring)
         self.overlap = True if overlap is None else bool(overlap)
-        # overlapped schedule without a halo: the slab's last local family takes
-        # d_z in its retire (STEP_XCHG) instead of a separate update pass
-        self.fused_last = False if fused_last is None else bool(fused_last)
         self._bufs = []
         for s, p in zip(self.slab, self.pencil):
             self._bufs.append(dict(Gs=self._tensor(s, N.BUF_G, np.float32),
@@ -322,14 +319,6 @@ class ShardedAAR:
             self._send_c = ([torch.empty((P, dz, cp), dtype=torch.float64, device=self._dev())
                              for _ in self.ranks] if not self.halo else None)
             self._streams = None
-            if not self.halo:
-                # the slab's last local family takes d_z and emits the new
-                # drift in its retire pass (STEP_XCHG): no separate update pass
-                for s, rv, sc in zip(self.slab, self._recv_s, self._send_c):
-                    if hasattr(s, "set_exchange_host"):
-                        s.set_exchange_host(rv.numpy(), sc.numpy(), P, dz, cp)
-                    else:
-                        s.set_exchange(rv.data_ptr(), sc.data_ptr(), P, dz, cp)
         if self.halo:
             self._hrow = [torch.empty(W, dtype=torch.float32, device=self._dev())
                           for _ in self.ranks]
@@ -494,10 +483,6 @@ class ShardedAAR:
             return torch.cuda.stream(st) if cuda else contextlib.nullcontext()
 
         acc_p = [torch.zeros_like(a) for a in acc]  # C-side partials (acc is S-side)
-        local = LOCAL[self.g.connectivity]
-        full = sum(1 << j for j in local)
-        head = full & ~(1 << local[-1])  # all local families but the last
-        fused = (not self.halo) and self.fused_last
         if cuda:
             base = torch.cuda.current_stream()
             S.wait_stream(base)
@@ -512,28 +497,15 @@ class ShardedAAR:
                     for i, p in enumerate(self.pencil):
                         p.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
                         acc_p[i][k] += self._bufs[i]["Np"][0]
-                    ev_p = torch.cuda.Event() if cuda else None
-                    if cuda and fused:
-                        ev_p.record(C)
                     self.comm.all_to_all([b["Gp"].view(P, dz, cp) for b in self._bufs],
                                          self._recv_s)
                     ev_a = torch.cuda.Event() if cuda else None
                     if cuda:
                         ev_a.record(C)
                 with on(S):  # local families while d_z is in flight
-                    if cuda and fused:
-                        # the pencil sweep first, then the slab's families while
-                        # d_z is exchanged: the last one needs it in its retire
-                        S.wait_event(ev_p)
                     for i, s in enumerate(self.slab):
-                        if not fused:
-                            s.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
-                            acc[i][k] += self._bufs[i]["Ns"][0]
-                        elif head:
-                            s.set_family_mask(head)
-                            s.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
-                            s.set_family_mask(full)
-                            acc[i][k] += self._bufs[i]["Ns"][0]
+                        s.step(1, N.STEP_NO_UPDATE | N.STEP_NORM_RAW, norms=False)
+                        acc[i][k] += self._bufs[i]["Ns"][0]
                     if self.halo:  # straddling paths' d on the halo row -> the owner's first row
                         self.comm.send_next(
                             [b["Gs"][ns:] if h else None for b, h in zip(self._bufs, has_halo)],
@@ -543,16 +515,7 @@ class ShardedAAR:
                                 b["Gs"][:W] += self._hrow[i]
                     if cuda:
                         S.wait_event(ev_a)
-                    if fused:
-                        # the last local family as LAST role: g = (G + d) + d_z, the
-                        # update, and the new drift into the send buffer, in its retire
-                        fl = (N.STEP_G_PRESET if head else 0) | N.STEP_XCHG | N.STEP_NORM_RAW
-                        for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
-                            s.set_family_mask(1 << local[-1])
-                            s.step(1, fl, norms=False)
-                            s.set_family_mask(full)
-                            acc[i][k] += b["Ns"][0]
-                    elif not self.halo:
+                    if not self.halo:
                         # one fused pass: g = G + d_z into the send buffer, and the update
                         for i, (s, b) in enumerate(zip(self.slab, self._bufs)):
                             if hasattr(s, "host_buffer"):

@@ -10,7 +10,7 @@ import numpy as np
 
 from oracle import oracle as orc
 
-STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW, STEP_XCHG = 1, 2, 4, 8, 16
+STEP_G_PRESET, STEP_NO_UPDATE, STEP_EXPORT_G, STEP_NORM_RAW = 1, 2, 4, 8
 BUF_G, BUF_X, BUF_C, BUF_Y, BUF_NORMS, BUF_BITS = 0, 1, 2, 3, 4, 6
 ORDER = {"2D-4": (0, 1), "2D-8": (0, 1, 2, 3), "3D-6": (0, 1, 2)}
 
@@ -101,16 +101,11 @@ class EmuSolver:
                     self.G[:] = (self.G.astype(np.float64) + d).astype(np.float32)
                 else:
                     g32 = (self.G.astype(np.float64) + d).astype(np.float32)
-                    if flags & STEP_XCHG:  # + the cross family's d (fp32 add), node order
-                        recv, send, P, dz, cp = self._xchg
-                        g32 = g32 + recv.reshape(P, dz, cp).transpose(1, 0, 2).reshape(-1)
                     g = g32.astype(np.float64)
                     xn = self.X.astype(np.float64) - g
                     self.X[:] = xn.astype(np.float32)
                     dcv = (xn - g) / self.r
                     self.c[:] = (z - pold.astype(np.float64)) + dcv
-                    if flags & STEP_XCHG:
-                        send.reshape(P, dz, cp)[...] = self.c.reshape(dz, P, cp).transpose(1, 0, 2)
                     if flags & STEP_EXPORT_G:
                         self.G[:] = g32
                     nrm += float(np.sum(2.0 * dcv * g + self.r * dcv * dcv))
@@ -129,10 +124,6 @@ class EmuSolver:
         self.c += dcv
         o = self.n_own
         self.norms[1] = float(np.sum(2.0 * dcv[:o] * gd[:o] + self.r * dcv[:o] * dcv[:o]))
-
-    def set_exchange_host(self, recv, send, P, dz, cp):
-        """pcb_set_exchange: buffers of STEP_XCHG steps (numpy views)."""
-        self._xchg = (recv, send, int(P), int(dz), int(cp))
 
     def apply_g_exchange_host(self, recv, send, P, dz, cp):
         """pcb_apply_g_exchange: g = G + d_z (fp32), apply_g, new drift into send [P][dz][cp]."""

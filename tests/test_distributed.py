@@ -32,8 +32,7 @@ def _worker(rank, world, port, conn, dims, iters, q, overlap=False):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = make_instance(SPEC[conn], seed=2, dims=dims)
-        sh = ShardedAAR(g, TorchComm(), [rank], EmuSolver, overlap=bool(overlap),
-                        fused_last=overlap == "fused")
+        sh = ShardedAAR(g, TorchComm(), [rank], EmuSolver, overlap=overlap)
         sh.init_cold()
         norms = sh.run(iters)
         parts = sh.local_z()
@@ -46,9 +45,7 @@ def _worker(rank, world, port, conn, dims, iters, q, overlap=False):
 
 @pytest.mark.parametrize("conn,dims,overlap", [("3D-6", (6, 8, 5), False), ("2D-4", (12, 10), False),
                                                ("2D-8", (12, 10), False), ("3D-6", (6, 8, 5), True),
-                                               ("2D-4", (12, 10), True), ("2D-8", (12, 10), True),
-                                               ("3D-6", (6, 8, 5), "fused"),
-                                               ("2D-4", (12, 10), "fused")])
+                                               ("2D-4", (12, 10), True), ("2D-8", (12, 10), True)])
 def test_gloo_world2_matches_unsharded(conn, dims, overlap):
     import multiprocessing as mp
     from emu import EmuSolver

@@ -8,23 +8,50 @@ import csv
 import sys
 from collections import defaultdict
 
-# fast_sweep.cuh line ranges (inclusive) -> section
-SECTIONS = [
-    ("cp/tma helpers", 125, 192), ("rcp/ring index", 193, 227),
-    ("lag/global", 236, 281), ("setup", 482, 639), ("issue", 640, 700),
-    ("prefetch G/X", 701, 729), ("to_z", 730, 738), ("retire", 739, 854),
-    ("scan trip", 855, 986), ("scan vote", 987, 999), ("main loop", 1095, 1143),
-    ("epilogue", 1144, 1161),
+# fast_sweep.cuh sections, located by their first line (the file as it is now:
+# re-run on a capture of the same source)
+MARKS = [
+    ("cp/tma helpers", "__device__ __forceinline__ void mbar_init"),
+    ("rcp/ring index", "__device__ __forceinline__ double rcp_small"),
+    ("lag/global", "__device__ __noinline__ double z_global"),
+    ("other fast_sweep", "struct Spec {"),
+    ("setup", "__global__ void __launch_bounds__(WARPS * 32)"),
+    ("issue", "  auto issue = [&](int T) {"),
+    ("prefetch G/X", "  auto prefetch = [&](int T) {"),
+    ("to_z", "  auto to_z = [&](int T) {"),
+    ("retire", "  auto retire = [&](int T) {"),
+    ("scan trip", "  auto scan = [&](int lo_pos"),
+    ("scan vote", "    for (;;) {\n      const int nact"),
+    ("VER", "  int ff = 0x7fffffff, fl = -1;"),
+    ("main loop", "  if (!VER && warp_live && rhi > 0) {"),
+    ("epilogue", "  if constexpr (VER) {\n    __syncwarp();"),
+    ("merge", "// Intra-chain split: merge points"),
 ]
+
+
+def _sections():
+    import os
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paracut_b200", "csrc",
+                            "fast_sweep.cuh")).read()
+    out = []
+    for name, mark in MARKS:
+        i = src.find(mark)
+        if i >= 0:
+            out.append((src.count("\n", 0, i) + 1, name))
+    return sorted(out)
+
+
+SECTIONS = _sections()
 
 
 def section(path, ln):
     if not path.endswith("fast_sweep.cuh"):
         return path.rsplit("/", 1)[-1]
-    for name, a, b in SECTIONS:
-        if a <= ln <= b:
-            return name
-    return "other fast_sweep"
+    name = "header"
+    for start, nm in SECTIONS:
+        if ln >= start:
+            name = nm
+    return name
 
 
 def main(path, n):

@@ -15,10 +15,9 @@ from paracut_b200.instances import CONFIGS, make_instance  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 g = make_instance(CONFIGS[wl], seed=0)
 r, n = len(g.dir_weights), g.n
-modes = [(False, False), (True, False), (True, True)]  # (overlap, fused last family)
-for P, (ov, fu) in [(P, m) for P in (1, 2, 4, 8) for m in modes]:
+for P, ov in [(P, ov) for P in (1, 2, 4, 8) for ov in (False, True)]:
     sh = ShardedAAR(g, LocalComm(P), range(P), lambda s: _native.GridSolver(s, precision="f32"),
-                    device="cuda", overlap=ov, fused_last=fu)
+                    device="cuda", overlap=ov)
     sh.init_cold()
     sh.run(3, norms=False)
     torch.cuda.synchronize()
@@ -34,6 +33,5 @@ for P, (ov, fu) in [(P, m) for P in (1, 2, 4, 8) for m in modes]:
     torch.cuda.synchronize()
     dg = (time.perf_counter() - t0) / 20
     print("%s P=%d virtual ranks on 1 GPU, %s: eager %.3f ms/iter, graph %.3f ms/iter (%.2e updates/s)"
-          % (wl, P, ("overlapped+fused" if fu else "overlapped") if ov else "serial",
-             dt * 1e3, dg * 1e3, r * n / dg))
+          % (wl, P, "overlapped" if sh.overlap else "serial", dt * 1e3, dg * 1e3, r * n / dg))
     del sh
