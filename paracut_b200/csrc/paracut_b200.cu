@@ -712,45 +712,64 @@ __global__ void __launch_bounds__(APPLY_THREADS, 3) k_apply_fast(
 
 // s = y_0 + y_1 + ... (class order), x = w - s, label bits per threshold,
 // partial sums: [unary_t (T)], dual, ww, dd.
-__global__ void k_check_nodes(const double* __restrict__ y, int r, const double* __restrict__ w,
-                              int64_t n, int64_t n_own, int T, const double* __restrict__ thr,
-                              uint8_t* __restrict__ bits, double* __restrict__ xcur,
-                              double* __restrict__ parts) {
-  double un[MAXT], th[MAXT];  // register arrays: every index below is static
+template <int TT, int R>  // threshold slots compiled in (TT = T, or MAXT generic); R families
+__global__ void __launch_bounds__(RED_BLOCK) k_check_nodes(
+    const double* __restrict__ y, const double* __restrict__ w, int64_t n, int64_t n_own, int T,
+    const double* __restrict__ thr, uint8_t* __restrict__ bits, double* __restrict__ xcur,
+    double* __restrict__ parts) {
+  double un[TT], th[TT];  // register arrays: every index below is static
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
+  for (int t = 0; t < TT; ++t) {
     un[t] = 0.0;
     th[t] = t < T ? thr[t] : 0.0;
   }
   double dual = 0.0, ww = 0.0, dd = 0.0;
-#pragma unroll 4
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double s = y[i];
-    for (int j = 1; j < r; ++j) s = s + y[(int64_t)j * n + i];
-    const double wi = w[i];
-    const double x = wi - s;
-    xcur[i] = x;
-    const bool own = i < n_own;  // halo copies: labels for the cut, sums are the owner's
-    unsigned b = 0;
+  // grid-stride over nodes, U strides at a time with every load of the U
+  // nodes issued before the arithmetic (the same nodes per thread, in the same
+  // order, as a plain grid-stride loop: the partial sums do not change)
+  constexpr int U = 4;
+  const int64_t step = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += U * step) {
+    double yv[U][R], wv[U];
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      if (t < T && x > th[t]) {
-        b |= 1u << t;
-        if (own) un[t] += wi;
-      }
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * step;
+      const bool ok = i < n;
+#pragma unroll
+      for (int j = 0; j < R; ++j) yv[u][j] = ok ? y[(int64_t)j * n + i] : 0.0;
+      wv[u] = ok ? w[i] : 0.0;
     }
-    bits[i] = (uint8_t)b;
-    if (!own) continue;
-    const double sw = s - wi;
-    dual += fmin(sw, 0.0);
-    ww += wi * wi;
-    dd += sw * sw;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * step;
+      if (i >= n) break;
+      double s = yv[u][0];
+#pragma unroll
+      for (int j = 1; j < R; ++j) s = s + yv[u][j];
+      const double wi = wv[u];
+      const double x = wi - s;
+      xcur[i] = x;
+      const bool own = i < n_own;  // halo copies: labels for the cut, sums are the owner's
+      unsigned b = 0;
+#pragma unroll
+      for (int t = 0; t < TT; ++t) {
+        if (t < T && x > th[t]) {
+          b |= 1u << t;
+          if (own) un[t] += wi;
+        }
+      }
+      bits[i] = (uint8_t)b;
+      if (!own) continue;
+      const double sw = s - wi;
+      dual += fmin(sw, 0.0);
+      ww += wi * wi;
+      dd += sw * sw;
+    }
   }
   __shared__ double sh[32];
   const int nv = T + 3;
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
+  for (int t = 0; t < TT; ++t) {
     if (t >= T) break;
     const double v = block_sum(un[t], sh);
     if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * nv + t] = v;
@@ -772,12 +791,13 @@ struct DirGeom {
 // One block walks whole grid rows (flattened leading coordinates); per row
 // and direction the edge-array row and the neighbour offset are computed
 // once, and the threads stride along the last axis (coalesced a_e and bits).
+template <int TT>
 __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_constant__ DirGeom DG,
                               const __grid_constant__ DirPtrs dw, const uint8_t* __restrict__ bits,
                               int T, double* __restrict__ parts) {
-  double cut[MAXT];
+  double cut[TT];
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) cut[t] = 0.0;
+  for (int t = 0; t < TT; ++t) cut[t] = 0.0;
   const int nd = D.nd;
   const int64_t L = nd == 3 ? D.d[2] : D.d[1];
   const int64_t rows = nd == 3 ? D.d[0] * D.d[1] : D.d[0];
@@ -839,7 +859,7 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
             if (diff && x >= loL && x < loL + lenL) {
               const double a = av[x];
 #pragma unroll
-              for (int t = 0; t < MAXT; ++t)
+              for (int t = 0; t < TT; ++t)
                 if ((diff >> t) & 1u) cut[t] += a;  // bits >= T are never set
             }
           }
@@ -852,7 +872,7 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
         if (diff) {
           const double a = av[x];
 #pragma unroll
-          for (int t = 0; t < MAXT; ++t)
+          for (int t = 0; t < TT; ++t)
             if ((diff >> t) & 1u) cut[t] += a;  // bits >= T are never set
         }
       }
@@ -860,7 +880,7 @@ __global__ void k_check_edges(const __grid_constant__ Dims D, const __grid_const
   }
   __shared__ double sh[32];
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
+  for (int t = 0; t < TT; ++t) {
     if (t >= T) break;
     const double v = block_sum(cut[t], sh);
     if (threadIdx.x == 0) parts[(int64_t)blockIdx.x * T + t] = v;
@@ -875,31 +895,49 @@ __global__ void k_labels(const uint8_t* bits, int64_t n, int t, uint8_t* lab) {
 
 // Jaccard distance of every logged packed labeling (slot i at lab + i * nb)
 // against ref: one block per slot, integer popcounts (exact).
-__global__ void k_log_jaccard(const uint8_t* lab, const uint8_t* ref, int64_t nb, double* out) {
-  const uint8_t* a = lab + (int64_t)blockIdx.x * nb;
+// Jaccard distance of every logged labeling against ref, in two steps: blocks
+// of grid (chunks, labelings) popcount one chunk of one labeling (8-byte words
+// when the rows are 8-byte aligned) and add their integer counts into the
+// labeling's (intersection, union) pair -- integer atomics, so the result is
+// independent of the order; k_log_jaccard_fin turns the pairs into distances.
+__global__ void k_log_jaccard_part(const uint8_t* __restrict__ lab, const uint8_t* __restrict__ ref,
+                                   int64_t nb, unsigned long long* __restrict__ acc) {
+  const uint8_t* a = lab + (int64_t)blockIdx.y * nb;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long inter = 0, uni = 0;
-  for (int64_t q = threadIdx.x; q < nb; q += blockDim.x) {
-    const unsigned x = a[q], y = ref[q];
-    inter += __popc(x & y);
-    uni += __popc(x | y);
+  if ((nb & 7) == 0) {
+    const unsigned long long* a8 = reinterpret_cast<const unsigned long long*>(a);
+    const unsigned long long* r8 = reinterpret_cast<const unsigned long long*>(ref);
+    const int64_t nw = nb >> 3;
+#pragma unroll 4
+    for (int64_t q = t0; q < nw; q += stride) {
+      const unsigned long long x = __ldg(a8 + q), y = __ldg(r8 + q);
+      inter += __popcll(x & y);
+      uni += __popcll(x | y);
+    }
+  } else {
+    for (int64_t q = t0; q < nb; q += stride) {
+      const unsigned x = a[q], y = ref[q];
+      inter += __popc(x & y);
+      uni += __popc(x | y);
+    }
   }
-  __shared__ unsigned long long si[32], su[32];
   for (int o = 16; o > 0; o >>= 1) {
     inter += __shfl_down_sync(0xffffffffu, inter, o);
     uni += __shfl_down_sync(0xffffffffu, uni, o);
   }
-  if ((threadIdx.x & 31) == 0) {
-    si[threadIdx.x >> 5] = inter;
-    su[threadIdx.x >> 5] = uni;
+  if ((threadIdx.x & 31) == 0 && (inter | uni)) {
+    atomicAdd(acc + 2 * blockIdx.y, inter);
+    atomicAdd(acc + 2 * blockIdx.y + 1, uni);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long ti = 0, tu = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
-      ti += si[w];
-      tu += su[w];
-    }
-    out[blockIdx.x] = tu == 0 ? 0.0 : 1.0 - (double)ti / (double)tu;
+}
+
+__global__ void k_log_jaccard_fin(const unsigned long long* acc, int64_t nlab, double* out) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nlab;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long ti = acc[2 * k], tu = acc[2 * k + 1];
+    out[k] = tu == 0 ? 0.0 : 1.0 - (double)ti / (double)tu;
   }
 }
 
@@ -1163,6 +1201,7 @@ struct pcb_solver {
   // programmatic dependent launch of the MID / LAST sweeps of a plain step
   // (PCB_PDL=0: off): their scans start in the previous sweep's tail, the
   // first read of its output waits in griddepcontrol.wait
+  DBuf<unsigned long long> jacc;  // (intersection, union) per logged labeling
   bool use_pdl = true;
   bool pdl_launch = false;  // the next launch_sweep is programmatic
   cudaStream_t side = nullptr;
@@ -1183,7 +1222,7 @@ struct pcb_solver {
   pcb_solver() {
     bind(w, z, y, p32, cdrift, X32, G32, tmp, yprev, bits, xcur, bestlab, bestx, parts, vals,
          norms, sp_cx, sp_fx, sp_cy, sp_fy, packed, normlog, lablog, merge, p32b, G32b, X32b,
-         cdriftb, vstate, p64, G64, X64, gnorms);
+         cdriftb, vstate, p64, G64, X64, gnorms, jacc);
     bind_arr(sg);
     bind_arr(dirw);
     bind_arr(dirw_base);
@@ -2900,16 +2939,48 @@ int pcb_check(pcb_solver* h, int nthr, const double* thr, double* energy, double
   const int g = grid_for(h->n, RED_BLOCK, NODE_GRID);
   const int nv = nthr + 3;
   h->x_in_best = false;  // (writes xcur afresh)
-  k_check_nodes<<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->r, h->w.p, h->n,
-                                                 h->n_own < 0 ? h->n : h->n_own, nthr,
-                                                 h->vals.p + 48,
-                                                 h->bits.p, h->xcur.p, h->parts.p);
+  // kernels with the threshold count compiled in for the usual 1..4 (fewer
+  // registers, full occupancy), the generic MAXT-slot kernels otherwise
+  auto nodes = [&](auto tt) {
+    constexpr int TT = decltype(tt)::value;
+    const int64_t own = h->n_own < 0 ? h->n : h->n_own;
+    if (h->r == 2)
+      k_check_nodes<TT, 2><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->w.p, h->n, own, nthr,
+                                                           h->vals.p + 48, h->bits.p, h->xcur.p,
+                                                           h->parts.p);
+    else if (h->r == 3)
+      k_check_nodes<TT, 3><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->w.p, h->n, own, nthr,
+                                                           h->vals.p + 48, h->bits.p, h->xcur.p,
+                                                           h->parts.p);
+    else
+      k_check_nodes<TT, 4><<<g, RED_BLOCK, 0, h->stream>>>(h->y.p, h->w.p, h->n, own, nthr,
+                                                           h->vals.p + 48, h->bits.p, h->xcur.p,
+                                                           h->parts.p);
+  };
+  switch (nthr) {
+    case 1: nodes(std::integral_constant<int, 1>()); break;
+    case 2: nodes(std::integral_constant<int, 2>()); break;
+    case 3: nodes(std::integral_constant<int, 3>()); break;
+    case 4: nodes(std::integral_constant<int, 4>()); break;
+    default: nodes(std::integral_constant<int, MAXT>()); break;
+  }
   LAUNCH_CHECK(h);
   k_reduce_cols<<<1, 32 * nv, 0, h->stream>>>(h->parts.p, g, nv, h->vals.p);
   LAUNCH_CHECK(h);
   DirPtrs dp{};
   for (int k = 0; k < h->DG.ndir; ++k) dp.p[k] = h->dirw[k].p;
-  k_check_edges<<<g, RED_BLOCK, 0, h->stream>>>(h->D, h->DG, dp, h->bits.p, nthr, h->parts.p);
+  auto edges = [&](auto tt) {
+    constexpr int TT = decltype(tt)::value;
+    k_check_edges<TT><<<g, RED_BLOCK, 0, h->stream>>>(h->D, h->DG, dp, h->bits.p, nthr,
+                                                      h->parts.p);
+  };
+  switch (nthr) {
+    case 1: edges(std::integral_constant<int, 1>()); break;
+    case 2: edges(std::integral_constant<int, 2>()); break;
+    case 3: edges(std::integral_constant<int, 3>()); break;
+    case 4: edges(std::integral_constant<int, 4>()); break;
+    default: edges(std::integral_constant<int, MAXT>()); break;
+  }
   LAUNCH_CHECK(h);
   k_reduce_cols<<<1, 32 * nthr, 0, h->stream>>>(h->parts.p, g, nthr, h->vals.p + 16);
   LAUNCH_CHECK(h);
@@ -3024,7 +3095,19 @@ int pcb_log_jaccard(pcb_solver* h, const uint8_t* ref_packed, double* out, int64
   if ((int64_t)h->parts.n < h->nlab)
     if (int e = h->parts.alloc(h->nlab)) return e;
   CUDA_TRY(hostio::h2d(h->packed.p, ref_packed, (size_t)nb, h->stream));
-  k_log_jaccard<<<(unsigned)h->nlab, 256, 0, h->stream>>>(h->lablog.p, h->packed.p, nb, h->parts.p);
+  if ((int64_t)h->jacc.n < 2 * h->nlab)
+    if (int e = h->jacc.alloc(2 * h->nlab)) return e;
+  CUDA_TRY(cudaMemsetAsync(h->jacc.p, 0, 2 * h->nlab * sizeof(unsigned long long), h->stream));
+  // chunks of about 64 KB per block, at most 65535 labelings per launch row
+  const unsigned chunks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(256, nb >> 16));
+  for (int64_t l0 = 0; l0 < h->nlab; l0 += 65535) {
+    const unsigned rows = (unsigned)std::min<int64_t>(65535, h->nlab - l0);
+    k_log_jaccard_part<<<dim3(chunks, rows), 256, 0, h->stream>>>(
+        h->lablog.p + l0 * nb, h->packed.p, nb, h->jacc.p + 2 * l0);
+    LAUNCH_CHECK(h);
+  }
+  k_log_jaccard_fin<<<grid_for(h->nlab, 256, 64), 256, 0, h->stream>>>(h->jacc.p, h->nlab,
+                                                                         h->parts.p);
   LAUNCH_CHECK(h);
   CUDA_TRY(hostio::d2h(out, h->parts.p, (size_t)h->nlab * sizeof(double), h->stream));
   CUDA_TRY(cudaStreamSynchronize(h->stream));
