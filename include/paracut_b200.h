@@ -112,6 +112,13 @@ int pcb_shape(const pcb_solver *h, int *r, int64_t *n);
 int pcb_set_stream(pcb_solver *h, uintptr_t stream);
 int pcb_synchronize(pcb_solver *h);
 
+/* A second handle of the same instance in another precision, built on the
+ * device from src's arrays (no host transfer), and the fused-form AAR state
+ * (f32 / f64s: p_j, drift c; x = w - sum_j p_j recomputed) moved between two
+ * such handles -- the f32 -> f64s hand-over of a polishing solve
+ * (solvers.py:150-165 warm start, without the host round trip of get_z/set_z). */
+int pcb_clone(const pcb_solver *src, int precision, pcb_solver **out);
+int pcb_copy_state(pcb_solver *dst, const pcb_solver *src);
 /* z0 = Pi_L(0) = w/r per class (solvers.py:284-285). */
 int pcb_init_cold(pcb_solver *h);
 /* Warm start / readback of the AAR point z, r*n fp64 class-major

@@ -53,6 +53,8 @@ def _declare(L):
     L.pcb_aar_run.argtypes = [P, I64, P]
     L.pcb_aar_step.argtypes = [P, I64, INT, P]
     L.pcb_set_family_mask.argtypes = [P, ctypes.c_uint]
+    L.pcb_clone.argtypes = [P, INT, ctypes.POINTER(P)]
+    L.pcb_copy_state.argtypes = [P, P]
     L.pcb_apply_g.argtypes = [P, ctypes.c_size_t]
     L.pcb_device_buffer.argtypes = [P, INT, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(I64)]
     L.pcb_shadow.argtypes = [P, P, P]
@@ -104,7 +106,7 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
            "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance",
-           "pcb_apply_g_exchange", "pcb_create_synthetic_box")
+           "pcb_apply_g_exchange", "pcb_create_synthetic_box", "pcb_clone", "pcb_copy_state")
 
 
 def lib():
@@ -255,6 +257,23 @@ class GridSolver:
         r, n = INT(0), I64(0)
         check(L.pcb_shape(h, ctypes.byref(r), ctypes.byref(n)))
         self.r, self.n = int(r.value), int(n.value)
+
+    def clone(self, precision):
+        """A handle of the same instance in another precision, built on the
+        device from this handle's arrays (pcb_clone); no AAR state yet."""
+        if precision not in PRECISIONS:
+            raise ValueError("precision must be one of %r" % (tuple(PRECISIONS),))
+        h = P()
+        check(lib().pcb_clone(self.handle, PRECISIONS[precision], ctypes.byref(h)))
+        other = GridSolver.__new__(GridSolver)
+        other.precision, other.device, other.dims = precision, self.device, self.dims
+        other._h, other.r, other.n = h, self.r, self.n
+        return other
+
+    def copy_state(self, src):
+        """The fused-form AAR state of another f32 / f64s handle of the same
+        instance, device to device (pcb_copy_state)."""
+        check(lib().pcb_copy_state(self.handle, src.handle))
 
     # -- lifecycle
     def close(self):

@@ -463,6 +463,31 @@ __global__ void k_set_fast(const double* z, ST* p, double* cdrift, ST* X, const 
   }
 }
 
+// Fused-form state of another handle of the same instance (pcb_copy_state):
+// p_j converted to this handle's state type element by element (the family
+// layouts are the same), the drift copied, x = w - sum_j p_j recomputed in
+// fp64 (the invariant the update keeps; zig-zag border nodes hold p = 0).
+template <class SS, class SD>
+__global__ void k_copy_fast(const SS* __restrict__ ps, const double* __restrict__ cs,
+                            SD* __restrict__ pd, double* __restrict__ cd, SD* __restrict__ X,
+                            const double* __restrict__ w, int64_t n, FamSet FS, Dims D) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double sp = 0.0;
+    for (int j = 0; j < FS.r; ++j) {
+      int64_t c;
+      int pos;
+      if (!fam_index(FS.f[j], D, i, &c, &pos)) continue;
+      const int64_t q = (int64_t)j * n + (int64_t)pos * FS.f[j].C + c;
+      const SD v = (SD)ps[q];
+      pd[q] = v;
+      sp += (double)v;
+    }
+    cd[i] = cs[i];
+    X[i] = (SD)(w[i] - sp);
+  }
+}
+
 template <class ST>
 __global__ void k_init_fast(ST* p, double* cdrift, ST* X, const double* w, int64_t n, int r) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -2183,6 +2208,7 @@ struct WeightSource {
   int fd = -1;            // file: payload at `off` (w, then each direction array)
   int64_t off = 0;
   const SynthSpec* syn = nullptr;
+  bool dev = false;       // w / dirw are device arrays on the same device (pcb_clone)
 };
 
 // the instance of a SynthSpec into h->w / h->dirw (stream 0, synchronous)
@@ -2343,7 +2369,9 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   if ((rc = h->w.alloc(n))) return bail(rc);
   int64_t foff = src.off;
   cudaError_t e = cudaSuccess;
-  if (!src.syn)
+  if (src.dev)
+    e = cudaMemcpy(h->w.p, src.w, n * sizeof(double), cudaMemcpyDeviceToDevice);
+  else if (!src.syn)
     e = src.fd >= 0 ? file_h2d(h->w.p, src.fd, foff, n * sizeof(double), 0)
                     : hostio::h2d(h->w.p, src.w, n * sizeof(double), 0);
   if (e != cudaSuccess) return bail(fail(PCB_E_CUDA, "upload w: %s", cudaGetErrorString(e)));
@@ -2351,7 +2379,11 @@ int create_impl(const int64_t* dims, int ndim, int conn, int precision, const We
   for (int k = 0; k < h->DG.ndir; ++k) {
     const int64_t cnt = dir_size(h, k);
     if ((rc = h->dirw[k].alloc(cnt))) return bail(rc);
-    if (cnt > 0 && !src.syn) {
+    if (cnt > 0 && src.dev) {
+      e = cudaMemcpy(h->dirw[k].p, src.dirw[k], cnt * sizeof(double), cudaMemcpyDeviceToDevice);
+      if (e != cudaSuccess)
+        return bail(fail(PCB_E_CUDA, "copy weights: %s", cudaGetErrorString(e)));
+    } else if (cnt > 0 && !src.syn) {
       if (src.fd >= 0) {
         bool neg = false;
         e = file_h2d(h->dirw[k].p, src.fd, foff, cnt * sizeof(double), 0, true, &neg);
@@ -2423,6 +2455,69 @@ int pcb_create(const int64_t* dims, int ndim, int conn, int precision, const dou
   src.w = w;
   src.dirw = dir_weights;
   return create_impl(dims, ndim, conn, precision, src, device, out);
+}
+
+int pcb_clone(const pcb_solver* src, int precision, pcb_solver** out) {
+  if (!src || !out) return fail(PCB_E_ARG, "null argument");
+  const double* dw[4] = {};
+  for (int k = 0; k < src->DG.ndir; ++k) dw[k] = src->dirw[k].p;
+  WeightSource ws;
+  ws.w = src->w.p;
+  ws.dirw = dw;
+  ws.dev = true;
+  int64_t dims[3];
+  for (int a = 0; a < src->D.nd; ++a) dims[a] = src->D.d[a];
+  if (int e = create_impl(dims, src->D.nd, src->conn, precision, ws, src->device, out)) return e;
+  pcb_solver* h = *out;
+  // a rescaled source keeps its lambda = 1 weights: so does the clone
+  for (int k = 0; k < src->DG.ndir; ++k) {
+    if (!src->dirw_base[k].p) continue;
+    const int64_t cnt = dir_size(h, k);
+    int e = h->dirw_base[k].alloc(cnt);
+    if (!e && cudaMemcpy(h->dirw_base[k].p, src->dirw_base[k].p, cnt * sizeof(double),
+                         cudaMemcpyDeviceToDevice) != cudaSuccess)
+      e = fail(PCB_E_CUDA, "copy base weights");
+    if (e) {
+      delete h;
+      *out = nullptr;
+      return e;
+    }
+  }
+  return 0;
+}
+
+int pcb_copy_state(pcb_solver* dst, const pcb_solver* src) {
+  if (!dst || !src) return fail(PCB_E_ARG, "null argument");
+  if (dst->n != src->n || dst->r != src->r || dst->conn != src->conn || dst->device != src->device)
+    return fail(PCB_E_ARG, "handles of different instances or devices");
+  const bool sf = src->precision == PCB_F32 || src->precision == PCB_F64S;
+  const bool df = dst->precision == PCB_F32 || dst->precision == PCB_F64S;
+  if (!sf || !df) return fail(PCB_E_ARG, "copy_state moves the fused-form state (f32 / f64s)");
+  if (!src->have_state) return fail(PCB_E_STATE, "no AAR state in the source");
+  if (int e = set_dev(dst)) return e;
+  CUDA_TRY(cudaStreamSynchronize(src->stream));  // the source's queued work first
+  const int g = grid_for(dst->n, 256, NODE_GRID);
+  const FamSet fs = famset(dst);
+  if (src->precision == PCB_F32 && dst->precision == PCB_F64S)
+    k_copy_fast<float, double><<<g, 256, 0, dst->stream>>>(src->p32.p, src->cdrift.p, dst->p64.p,
+        dst->cdrift.p, dst->X64.p, dst->w.p, dst->n, fs, dst->D);
+  else if (src->precision == PCB_F32)
+    k_copy_fast<float, float><<<g, 256, 0, dst->stream>>>(src->p32.p, src->cdrift.p, dst->p32.p,
+        dst->cdrift.p, dst->X32.p, dst->w.p, dst->n, fs, dst->D);
+  else if (dst->precision == PCB_F64S)
+    k_copy_fast<double, double><<<g, 256, 0, dst->stream>>>(src->p64.p, src->cdrift.p,
+        dst->p64.p, dst->cdrift.p, dst->X64.p, dst->w.p, dst->n, fs, dst->D);
+  else
+    k_copy_fast<double, float><<<g, 256, 0, dst->stream>>>(src->p64.p, src->cdrift.p,
+        dst->p32.p, dst->cdrift.p, dst->X32.p, dst->w.p, dst->n, fs, dst->D);
+  LAUNCH_CHECK(dst);
+  if (dst->precision == PCB_F32)
+    if (int e = reset_verify(dst)) return e;
+  CUDA_TRY(cudaStreamSynchronize(dst->stream));
+  dst->have_state = true;
+  dst->have_shadow = false;
+  dst->alg = 0;
+  return 0;
 }
 
 int pcb_create_from_file(const char* path, int precision, int device, pcb_solver** out,

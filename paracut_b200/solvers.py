@@ -417,9 +417,13 @@ def solve_aar(g, dec, cfg, _solver=None, _resident=False, _make64=None):
         # fp32 state leaves a ~1e-5 floor on the discrete gap of large instances;
         # continue in fp64 (the split fast kernels by default) from the same
         # AAR point to certify
-        S64 = (_make64() if _make64 is not None else
-               _native.GridSolver(g, precision=cfg.polish_precision, device=cfg.device))
-        S64.set_z(S.get_z())
+        # the polish handle is built from the f32 one on the device, and the
+        # state moves over device to device (no host round trip)
+        S64 = _make64() if _make64 is not None else S.clone(cfg.polish_precision)
+        if cfg.polish_precision == "f64s":
+            S64.copy_state(S)
+        else:  # the bitwise kernels keep z_j themselves
+            S64.set_z(S.get_z())
         drv.switch_solver(S64)
         drv.kmax = k + cfg.polish_iters
         drv.record("polish_start", k)
@@ -513,10 +517,8 @@ def solve_path(g, lambdas, cfg, keep_states=True):
         gl = _ScaledGrid(g, lam)
         c = cfg if i == 0 else dataclasses.replace(cfg, warm_start=None, force_warm=True)
 
-        def make64(lam=lam):
-            T = _native.GridSolver(g, precision=cfg.polish_precision, device=cfg.device)
-            T.scale_pairwise(lam)
-            return T
+        def make64():  # S holds this lambda's weights: the clone copies them
+            return S.clone(cfg.polish_precision)
         res = solve_aar(gl, GridDecomposition(gl), c, _solver=S, _resident=i > 0,
                         _make64=make64)
         if i + 1 < len(lambdas):  # the device state moves on: freeze this step's

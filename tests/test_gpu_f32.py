@@ -209,3 +209,33 @@ def test_f64s_within_1e6_of_oracle(conn, dims, k):
     assert _rel(x, x_ref) <= 1e-6
     assert _rel(res.dual_state.z, z_ref) <= 1e-6
     assert np.allclose(res.monitor["aar_step_norm"], norms_ref, rtol=1e-6, atol=1e-9)
+
+
+def test_clone_and_copy_state_device_handover():
+    """pcb_clone + pcb_copy_state: the f64s handle built on the device from an
+    f32 one carries the same instance and exactly the same z (p_j converted,
+    drift copied), and its iterations match a host round trip (get_z/set_z)."""
+    from paracut_b200 import _native
+    from paracut_b200.instances import synth_image, energy_from_image
+    g = energy_from_image(synth_image((40, 36, 28), 6, 3, 9, seed=7), "3D-6")
+    S = _native.GridSolver(g, precision="f32")
+    S.init_cold()
+    S.run(30, norms=False)
+    T = S.clone("f64s")
+    T.copy_state(S)
+    assert np.array_equal(T.get_z(), S.get_z())
+    U = _native.GridSolver(g, precision="f64s")
+    U.set_z(S.get_z())
+    T.run(20, norms=False)
+    U.run(20, norms=False)
+    zt, zu = T.get_z(), U.get_z()
+    assert np.max(np.abs(zt - zu)) <= 1e-9 * np.max(np.abs(zu))
+    # the clone of a rescaled handle keeps the lambda = 1 weights as its base
+    S.scale_pairwise(2.0)
+    V = S.clone("f64s")
+    V.scale_pairwise(1.0)
+    W = _native.GridSolver(g, precision="f64s")
+    for h in (V, W):
+        h.init_cold()
+        h.run(5, norms=False)
+    assert np.array_equal(V.get_z(), W.get_z())
