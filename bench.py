@@ -535,7 +535,7 @@ def main():
 
     ttc = None
     if rank == 0 and world == 1 and not args.no_ttc:
-        ttc = time_to_cut(pc, g, precision, local)
+        ttc = time_to_cut(pc, gp if not args.no_e2e else g, precision, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
