@@ -752,10 +752,21 @@ __global__ void __launch_bounds__(WARPS * 32)
   };
 
   // lockstep retire of tile T: per-node outputs from (z, segment markers), write back
-  auto retire = [&](int T) {
-    PCB_CNT(4, 1);
-    if (pre_tile != T) prefetch(T);
+  // (HINTS: this sweep writes segment hints -- a separate instantiation of the
+  // per-position body, so the common case carries no hint arithmetic)
+  // FULL: every lane emitted the whole tile (the usual case), so the
+  // per-position emit tests go
+  auto retire_impl = [&](int T, auto hints_tag, auto full_tag) {
+    constexpr bool HINTS = decltype(hints_tag)::value;
+    constexpr bool FULL = decltype(full_tag)::value;
     const int k0 = T * TP;
+    // the tile's output rows: p' in the family layout (32-bit element index),
+    // G / X / c in node order
+    const int pi0 = k0 * C32 + c32;
+    const int nd0 = node(base32, k0);
+    // strided families: the tile's ring rows are 32 slots apart from a per-tile
+    // base, so every per-position ring access is base + immediate
+    const int ixb = ROWLIKE ? 0 : pix(lane, k0);
     // positions of this tile my chain emitted: [max(start, k0), min(stop, i0))
     const int elo = max(start, k0) - k0, ehi = min(min(stop, i0), k0 + TP) - k0;
     const unsigned emask = (has && ehi > elo) ? (((1u << ehi) - 1u) & ~((1u << elo) - 1u)) : 0u;
@@ -765,8 +776,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
       double& nq = (q & 1) ? nb : na;
-      if ((emask >> q) & 1u) {
-        const int ix = tix(k0, q);
+      if (FULL || ((emask >> q) & 1u)) {
+        const int ix = ROWLIKE ? rix(lane, pos) : ixb + (q << 5);
         const double zj = rz[ix];
         if ((stile >> q) & 1u) {
           zs = zj;
@@ -775,7 +786,7 @@ __global__ void __launch_bounds__(WARPS * 32)
             qs = __hiloint2double(__float_as_int((float)ra[ix]), __float_as_int((float)rp[ix]));
           else
             qs = (double)ra[ix];
-          if (SGW) {
+          if (HINTS) {
             // the segment's prox value; jumps below 1e-6 (fp32 rounding of q)
             // count as none, so the change count sees segmentation changes
             // rather than rounding noise
@@ -797,9 +808,9 @@ __global__ void __launch_bounds__(WARPS * 32)
           const ST dS = p32 - pold;
           const double d = (double)dS;
           nq = nrm_d(d, nq);
-          A.po[(pos * C32 + c32)] = p32;
+          A.po[pi0 + q * C32] = p32;
           if (!ROWLIKE) {
-            const int nd = node(base32, pos);
+            const int nd = nd0 + q * ns32;  // strided: node(base32, k0 + q)
             if (ROLE == FIRST) {
               A.G[nd] = dS;
             } else if (ROLE == MID) {
@@ -821,7 +832,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
     }
     smask &= ~(0xffu << ((k0 & (RL - 1))));
-    if (SGW && valid) {
+    if (HINTS && valid) {
       // the word of tile T - 1 is complete now (its last edge's side came from
       // a segment start at k0); the old word of tile T is read for the next one
       hold_prev = hold_cur;
@@ -841,9 +852,9 @@ __global__ void __launch_bounds__(WARPS * 32)
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
-        const unsigned em_i = __shfl_sync(0xffffffffu, emask, i);
+        const unsigned em_i = FULL ? 0xffu : __shfl_sync(0xffffffffu, emask, i);
         const int bi = bB[ib];
-        if ((em_i >> q) & 1u) {
+        if (FULL || ((em_i >> q) & 1u)) {
           const int ix = rx(i, pos);
           const int nd = node(bi, pos);
           if (ROLE == SHADOW) {
@@ -868,6 +879,15 @@ __global__ void __launch_bounds__(WARPS * 32)
       __syncwarp();
     }
     nrm += na + nb;
+  };
+  auto retire = [&](int T) {
+    PCB_CNT(4, 1);
+    if (pre_tile != T) prefetch(T);
+    const int k0 = T * TP;
+    const bool full = has && max(start, k0) == k0 && min(min(stop, i0), k0 + TP) == k0 + TP;
+    if (SGW) retire_impl(T, std::true_type(), std::false_type());
+    else if (__all_sync(0xffffffffu, full)) retire_impl(T, std::false_type(), std::true_type());
+    else retire_impl(T, std::false_type(), std::false_type());
   };
 
   // one round of scanning; LAG: some lane's anchor is below the ring
