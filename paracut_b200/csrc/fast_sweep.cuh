@@ -177,6 +177,13 @@ __device__ __forceinline__ void cp_elem(void* dst, const T* src, bool pred) {
   if (sizeof(T) == 8) cp8(dst, src, pred);
   else cp4(dst, src, pred);
 }
+// unpredicated forms with a 32-bit shared address (the whole-tile issue path)
+__device__ __forceinline__ void cp4s(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp8s(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+}
 __device__ __forceinline__ void l2_prefetch(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -506,10 +513,14 @@ __global__ void __launch_bounds__(WARPS * 32)
   // block); row-like families keep [lane][pos] with the XOR swizzle that
   // their 8-lanes-along-a-row loads need
   auto rx = [](int l, int pos) { return ROWLIKE ? rix(l, pos) : pix(l, pos); };
+  const unsigned rz_s = (unsigned)__cvta_generic_to_shared(rz);
+  const unsigned rp_s = (unsigned)__cvta_generic_to_shared(rp);
+  const unsigned ra_s = (unsigned)__cvta_generic_to_shared(ra);
   // ring index of position k0 + q of a tile (k0 a multiple of TP, q < TP): in
   // the [pos][lane] layout the tile's rows are 32 apart with no wrap inside a
   // tile, so the per-q offset folds into the shared-memory address immediate
-  auto tix = [&](int k0, int q) { return ROWLIKE ? rix(lane, k0 + q) : pix(lane, k0) + (q << 5); };
+  // (row-like: k0 is a multiple of TP = 8, so slot (k0 + q) ^ swizzle = slot(k0) ^ q)
+  auto tix = [&](int k0, int q) { return ROWLIKE ? (rix(lane, k0) ^ q) : pix(lane, k0) + (q << 5); };
   const bool use_tma = !ROWLIKE && M.tma;
   unsigned long long* mbar =
       reinterpret_cast<unsigned long long*>(base + 32 * RL * (8 + 2 * sizeof(ST)));
@@ -678,6 +689,43 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
       return;
     }
+    if (k0 + TP < m && nvalid == 32) {
+      // whole tile of a full warp (the usual case): every position has a weight
+      // and every lane a chain, so no per-copy predicates; shared addresses are
+      // a per-tile base XOR / + an immediate (the ring rows of a tile: row-like
+      // slot (k0 + q) ^ swizzle = slot(k0) ^ q, strided rows 32 slots apart)
+      const unsigned bx = ROWLIKE ? (unsigned)rix(lane, k0) : (unsigned)pix(lane, k0);
+      const unsigned P0 = rp_s + bx * (unsigned)sizeof(ST), A0 = ra_s + bx * (unsigned)sizeof(ST);
+      const unsigned Z0 = rz_s + bx * 8u;
+      const int fi0 = k0 * C32 + c32;
+      const ST* const gp = A.p;
+      const ST* const ga = A.wf;
+#pragma unroll
+      for (int q = 0; q < TP; ++q) {
+        const unsigned o = ROWLIKE ? ((unsigned)q * (unsigned)sizeof(ST)) : 0u;
+        const unsigned so = ROWLIKE ? 0u : (unsigned)(q << 5) * (unsigned)sizeof(ST);
+        const int fi = fi0 + q * C32;
+        if (sizeof(ST) == 8) {
+          cp8s(ROWLIKE ? (P0 ^ o) : P0 + so, gp + fi);
+          cp8s(ROWLIKE ? (A0 ^ o) : A0 + so, ga + fi);
+        } else {
+          cp4s(ROWLIKE ? (P0 ^ o) : P0 + so, gp + fi);
+          cp4s(ROWLIKE ? (A0 ^ o) : A0 + so, ga + fi);
+        }
+        if (!ROWLIKE) cp8s(Z0 + (unsigned)(q << 5) * 8u, A.c + (base32 + (k0 + q) * ns32));
+      }
+      if (ROWLIKE) {  // mode B: lanes 8g..8g+7 along chain rows {8g + ib}
+        const int pos = k0 + (lane & 7);
+        const int poff = pos * ns32 + zz32 * ((pos + ph32) & 1);
+        const int gb = (lane >> 3) << 3;
+        const double* const cg = A.c;
+#pragma unroll
+        for (int ib = 0; ib < 8; ++ib)
+          cp8s(rz_s + (unsigned)(rix(gb, pos) ^ (ib * 33)) * 8u, cg + (unsigned)(bB[ib] + poff));
+      }
+      cp_commit();
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < TP; ++q) {  // mode A
       const int pos = k0 + q;
@@ -766,7 +814,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int nd0 = node(base32, k0);
     // strided families: the tile's ring rows are 32 slots apart from a per-tile
     // base, so every per-position ring access is base + immediate
-    const int ixb = ROWLIKE ? 0 : pix(lane, k0);
+    const int ixb = ROWLIKE ? rix(lane, k0) : pix(lane, k0);
     // positions of this tile my chain emitted: [max(start, k0), min(stop, i0))
     const int elo = max(start, k0) - k0, ehi = min(min(stop, i0), k0 + TP) - k0;
     const unsigned emask = (has && ehi > elo) ? (((1u << ehi) - 1u) & ~((1u << elo) - 1u)) : 0u;
@@ -777,7 +825,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       const int pos = k0 + q;
       double& nq = (q & 1) ? nb : na;
       if (FULL || ((emask >> q) & 1u)) {
-        const int ix = ROWLIKE ? rix(lane, pos) : ixb + (q << 5);
+        const int ix = ROWLIKE ? (ixb ^ q) : ixb + (q << 5);
         const double zj = rz[ix];
         if ((stile >> q) & 1u) {
           zs = zj;
@@ -849,13 +897,15 @@ __global__ void __launch_bounds__(WARPS * 32)
       __syncwarp();
       const int q = lane & 7;
       const int pos = k0 + q;
+      // ring slot of row gb + ib at pos: rix(gb, pos) ^ (ib * 33) (gb a multiple of 8)
+      const int rgb = rix((lane >> 3) << 3, pos);
 #pragma unroll
       for (int ib = 0; ib < 8; ++ib) {
         const int i = ((lane >> 3) << 3) + ib;
         const unsigned em_i = FULL ? 0xffu : __shfl_sync(0xffffffffu, emask, i);
         const int bi = bB[ib];
         if (FULL || ((em_i >> q) & 1u)) {
-          const int ix = rx(i, pos);
+          const int ix = rgb ^ (ib * 33);
           const int nd = node(bi, pos);
           if (ROLE == SHADOW) {
             A.y[nd] = rz[ix];
