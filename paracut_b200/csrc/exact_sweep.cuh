@@ -176,6 +176,21 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
   // lockstep retire of tile T: y = z - fill for every emitted position
   auto retire = [&](int T) {
     const int k0 = T * TP;
+    // every lane emitted the whole tile (the usual case): straight-line, ring
+    // slots rix(k0) ^ q, strided outputs at a per-tile base + q * ns
+    if (__all_sync(0xffffffffu, valid && k0 + TP <= m && k0 + TP <= i0)) {
+      const int ixb = rix(lane, k0);
+      const unsigned stile = smask >> (k0 & (RL - 1));
+      double* const yb = ROWLIKE ? nullptr : A.y + fam_node(F, my_base, k0);
+#pragma unroll
+      for (int q = 0; q < TP; ++q) {
+        const int ix = ixb ^ q;
+        if ((stile >> q) & 1u) fcarry = ra[ix];
+        const double yv = rz[ix] - fcarry;
+        if (!ROWLIKE) yb[(int64_t)q * F.ns] = yv;
+        else rz[ix] = yv;
+      }
+    } else {
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
@@ -186,6 +201,7 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
         if (!ROWLIKE) A.y[fam_node(F, my_base, pos)] = yv;
         else rz[ix] = yv;
       }
+    }
     }
     smask &= ~(((1u << TP) - 1u) << (k0 & (RL - 1)));
     if (ROWLIKE) {
