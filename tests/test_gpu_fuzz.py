@@ -1,8 +1,8 @@
 """Randomized shapes and weights through both device paths against the C
 oracle: odd and degenerate dims (partial warps, one-node chains, chains
 shorter than a tile), zero weights (piece ends), integer data, forced
-intra-chain splits and TMA / cp.async families.  f64 is bitwise, f32 within
-the north_star tolerance."""
+intra-chain splits and TMA / cp.async families.  f64 is bitwise, f32 and
+f64s within the north_star tolerances (1e-4, 1e-6)."""
 import numpy as np
 import pytest
 
@@ -47,6 +47,10 @@ def test_random_instances_both_paths(monkeypatch, oracle_lib, seed):
     x = g.w - r32.dual_state.y.sum(axis=0)
     scale = max(float(np.max(np.abs(x_ref))), 1.0)
     assert float(np.max(np.abs(x - x_ref))) <= 1e-4 * scale, (g.connectivity, g.dims, k)
+    # the fast fp64 mode (split chains, fp64 state and scans): 1e-6
+    r64s = pc.solve(g, dec, pc.SolverConfig(max_iters=k, check_every=k + 1, precision="f64s"))
+    xs = g.w - r64s.dual_state.y.sum(axis=0)
+    assert float(np.max(np.abs(xs - x_ref))) <= 1e-6 * scale, (g.connectivity, g.dims, k)
     # checks every few iterations: the check-iteration update (tiled apply)
     # runs on non-zero states of every family layout
     ce = int(rng.integers(1, 5))
