@@ -792,11 +792,18 @@ __global__ void __launch_bounds__(WARPS * 32)
 
   // tile T landed: c slot -> z = p + c (lockstep)
   auto to_z = [&](int T) {
+    // every load of the tile first, then the stores: the compiler cannot tell
+    // the ring arrays apart, so an interleaved form serialises load -> store
+    ST pv[TP];
+    double cv[TP];
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int ix = tix(T * TP, q);
-      rz[ix] = (double)rp[ix] + rz[ix];
+      pv[q] = rp[ix];
+      cv[q] = rz[ix];
     }
+#pragma unroll
+    for (int q = 0; q < TP; ++q) rz[tix(T * TP, q)] = (double)pv[q] + cv[q];
   };
 
   // lockstep retire of tile T: per-node outputs from (z, segment markers), write back

@@ -19,7 +19,7 @@ MARKS = [
     ("issue", "  auto issue = [&](int T) {"),
     ("prefetch G/X", "  auto prefetch = [&](int T) {"),
     ("to_z", "  auto to_z = [&](int T) {"),
-    ("retire", "  auto retire = [&](int T) {"),
+    ("retire", "  auto retire_impl = [&](int T"),
     ("scan trip", "  auto scan = [&](int lo_pos"),
     ("scan vote", "    for (;;) {\n      const int nact"),
     ("VER", "  int ff = 0x7fffffff, fl = -1;"),
