@@ -827,6 +827,11 @@ __global__ void __launch_bounds__(WARPS * 32)
     const unsigned emask = (has && ehi > elo) ? (((1u << ehi) - 1u) & ~((1u << elo) - 1u)) : 0u;
     double na = 0.0, nb = 0.0;  // two monitor accumulators: shorter dependency chains
     const unsigned stile = smask >> (k0 & (RL - 1));  // segment starts of this tile (bit q)
+    // row-like values for the ring (d, or the shadow's y) are stored after the
+    // loop: the compiler cannot tell the ring arrays apart, so a store inside
+    // it would order every later ring load behind it
+    ST dsv[TP];
+    double ysv[TP];
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
@@ -854,7 +859,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const double pn = (zj - zs) + qs;
         if (ROLE == SHADOW) {
           if (!ROWLIKE) A.y[node(base32, pos)] = pn;
-          else rz[ix] = pn;
+          else ysv[q] = pn;
         } else {
           const ST pold = rp[ix];
           const ST p32 = (ST)pn;
@@ -881,8 +886,17 @@ __global__ void __launch_bounds__(WARPS * 32)
               nq = nrm_last(dcv, g, A.rd, nq);
             }
           } else {
-            ra[ix] = dS;
+            dsv[q] = dS;
           }
+        }
+      }
+    }
+    if (ROWLIKE) {
+#pragma unroll
+      for (int q = 0; q < TP; ++q) {
+        if (FULL || ((emask >> q) & 1u)) {
+          if (ROLE == SHADOW) rz[ixb ^ q] = ysv[q];
+          else ra[ixb ^ q] = dsv[q];
         }
       }
     }
