@@ -182,13 +182,19 @@ __device__ __forceinline__ void sweep_warp(const Args& A, unsigned char* base, i
       const int ixb = rix(lane, k0);
       const unsigned stile = smask >> (k0 & (RL - 1));
       double* const yb = ROWLIKE ? nullptr : A.y + fam_node(F, my_base, k0);
+      // (row-like: the ring stores after the loop, so the loop's ring loads
+      // are not ordered behind them)
+      double yq[TP];
 #pragma unroll
       for (int q = 0; q < TP; ++q) {
         const int ix = ixb ^ q;
         if ((stile >> q) & 1u) fcarry = ra[ix];
-        const double yv = rz[ix] - fcarry;
-        if (!ROWLIKE) yb[(int64_t)q * F.ns] = yv;
-        else rz[ix] = yv;
+        yq[q] = rz[ix] - fcarry;
+        if (!ROWLIKE) yb[(int64_t)q * F.ns] = yq[q];
+      }
+      if (ROWLIKE) {
+#pragma unroll
+        for (int q = 0; q < TP; ++q) rz[ixb ^ q] = yq[q];
       }
     } else {
 #pragma unroll
