@@ -1339,10 +1339,20 @@ __global__ void __launch_bounds__(MWARPS * 32) k_merge(Fam F, const ST* p, const
   cp_commit();
   cp_wait(0);
   __syncwarp();
-#pragma unroll 4
-  for (int q = 0; q < MW; ++q) {
-    const int ix = mix(lane, q);
-    z_s[ix] = (double)p_s[ix] + z_s[ix];
+  // z = p + c in chunks of 8 positions, loads before stores (the compiler
+  // cannot tell the staging arrays apart and would serialise load -> store)
+#pragma unroll
+  for (int q0 = 0; q0 < MW; q0 += 8) {
+    ST pv[8];
+    double cv[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int ix = mix(lane, q0 + q);
+      pv[q] = p_s[ix];
+      cv[q] = z_s[ix];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) z_s[mix(lane, q0 + q)] = (double)pv[q] + cv[q];
   }
   __syncwarp();
   if (!valid) return;
