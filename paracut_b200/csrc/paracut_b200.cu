@@ -1231,6 +1231,11 @@ struct pcb_solver {
   bool pdl_launch = false;  // the next launch_sweep is programmatic
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_merge[MAXR] = {};
+  // recorded right after the previous step's last sweep: the next step's
+  // merges need only that (not the norm reduction queued behind it).  Valid
+  // only between steps of one pcb_aar_step call outside graph boundaries.
+  cudaEvent_t ev_sweeps = nullptr;
+  bool sweeps_ev_ok = false;
   // profiling: event pairs around family launches
   bool profiling = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -1257,6 +1262,7 @@ struct pcb_solver {
   ~pcb_solver() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     if (ev_start) cudaEventDestroy(ev_start);
+    if (ev_sweeps) cudaEventDestroy(ev_sweeps);
     for (cudaEvent_t e : ev_merge)
       if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
@@ -1734,6 +1740,7 @@ int ensure_side(pcb_solver* h) {
   if (h->side) return 0;
   CUDA_TRY(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->ev_sweeps, cudaEventDisableTiming));
   for (int j = 0; j < MAXR; ++j)
     CUDA_TRY(cudaEventCreateWithFlags(&h->ev_merge[j], cudaEventDisableTiming));
   return 0;
@@ -1919,8 +1926,12 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     for (int q = 0; q < na; ++q) any = any || h->nbk[act[q]] > 1;
     if (any) {
       if (int e = ensure_side(h)) return e;
-      CUDA_TRY(cudaEventRecord(h->ev_start, h->stream));
-      CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_start, 0));
+      if (h->sweeps_ev_ok) {  // the previous step's sweeps only
+        CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_sweeps, 0));
+      } else {
+        CUDA_TRY(cudaEventRecord(h->ev_start, h->stream));
+        CUDA_TRY(cudaStreamWaitEvent(h->side, h->ev_start, 0));
+      }
       for (int q = 0; q < na; ++q) {
         const int j = act[q];
         if (h->nbk[j] <= 1) continue;
@@ -1999,6 +2010,10 @@ int step_fast(pcb_solver* h, double* norm_slot, int flags) {
     prof_end(h);
     if (rc) return rc;
     off += fam_units(h, j);
+  }
+  if (h->side && h->ev_sweeps) {  // the next step's merges may start here
+    CUDA_TRY(cudaEventRecord(h->ev_sweeps, h->stream));
+    h->sweeps_ev_ok = true;
   }
   if (dbuf) {
     VModeArgs va{};
@@ -2868,6 +2883,7 @@ int graph_steps(pcb_solver* h) {
     h->stream = h->gstream;
     cudaGraph_t graph = nullptr;
     CUDA_TRY(cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
+    h->sweeps_ev_ok = false;  // the graph's first step orders on its own start
     int rc = 0;
     const int par0 = h->par;
     for (int k = 0; k < GRAPH_STEPS && !rc; ++k) rc = one_step(h, h->gnorms.p + k, 0);
@@ -2912,11 +2928,13 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
     if (int e = grow_keep(h->normlog, (size_t)(h->nlog + iters), (size_t)h->nlog, h->stream, 4096))
       return e;
   double* nout = to_log ? h->normlog.p + h->nlog : h->norms.p;
+  h->sweeps_ev_ok = false;  // other work may have touched the state since the last step
   const bool use_graph = flags == 0 && !h->profiling && graphs_enabled() && h->precision != PCB_F64;
   int64_t k = 0;
   if (use_graph)
     for (; k + GRAPH_STEPS <= iters; k += GRAPH_STEPS) {
       if (int rc = graph_steps(h)) return rc;
+      h->sweeps_ev_ok = false;  // (recorded inside the capture, not at this replay)
       CUDA_TRY(cudaMemcpyAsync(nout + k, h->gnorms.p, GRAPH_STEPS * sizeof(double),
                                cudaMemcpyDeviceToDevice, h->stream));
     }
