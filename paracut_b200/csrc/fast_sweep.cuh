@@ -116,10 +116,17 @@ inline void args_inplace(ArgsT<ST>& a) {
 // their ring tiles -- p_j and the weights (interleaved [pos][C]) and the
 // drift c (natural layout) -- as (32 chains x 8 positions) boxes, one
 // instruction per array per tile, completing on a per-tile mbarrier.
+//
+// Row families (2D rows, 3D x lines: a chain is one contiguous row of the
+// node arrays) with row = 1: p_j and the weights as above, and the drift as
+// a (8 positions x 32 rows) box of the natural layout, 64-B swizzled, landing
+// in the tile's z slots as [row][pos]; to_z transposes it to the ring's
+// [pos][lane] layout (k_sweep<..., RT = true>).
 struct Maps {
   CUtensorMap p, a, c;
   int tma;      // 1: use the maps (else cp.async per lane)
   int c3;       // the c map is 3D: (x = c % cdiv, pos, c / cdiv)
+  int row;      // row family: the c map is (pos, row), SWIZZLE_64B
 };
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -236,8 +243,9 @@ template <int ROLE, class ST = float>
 __host__ __device__ constexpr int ring_bytes_host() {
   // rz f64, rp / ra one state element each (an fp32 SHADOW keeps its fp64
   // segment values split over the dead rp / ra slots), + NT tile mbarriers,
-  // padded to 128 B so every warp's tile slots stay TMA-aligned
-  return 32 * RL * (8 + 2 * (int)sizeof(ST)) + 128;
+  // padded to 512 B so every warp's tile slots stay aligned to the 64-B
+  // swizzle atom of the row families' drift boxes
+  return (32 * RL * (8 + 2 * (int)sizeof(ST)) + 128 + 511) & ~511;
 }
 
 // lagging-lane accessors (positions below the ring), kept out of line
@@ -486,12 +494,17 @@ __device__ __noinline__ double repair_lane(const Args& A, int c32, int base32, i
   return nrm;
 }
 
-template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float>
+// RT: a row family fed by TMA (Maps::row); it runs the strided families'
+// [pos][lane] ring (ROWLIKE = false), with the drift box transposed in to_z
+// and its node-order outputs stored as per-lane vectors along the row.
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false>
 __global__ void __launch_bounds__(WARPS * 32)
     k_sweep(const __grid_constant__ ArgsT<ST> A, const __grid_constant__ Maps M) {
   static_assert(!VER || sizeof(ST) == 4, "verified sweeps run in the fp32-state mode");
+  static_assert(!RT || (!ROWLIKE && !VER && (ROLE == FIRST || ROLE == SHADOW)),
+                "row-TMA sweeps: first family or shadow only");
   constexpr bool S64 = sizeof(ST) == 8;  // fp64 state (f64s): fp64 scan, fp64 ring slots
-  extern __shared__ __align__(128) unsigned char smem_raw[];  // TMA boxes land 128-B aligned
+  extern __shared__ __align__(1024) unsigned char smem_raw[];  // TMA boxes land 512-B aligned
   // device-side choice between the two sweeps of a family (both are launched;
   // the one the mode word does not select returns at once)
   if (A.vmode != nullptr && ((*A.vmode == 1) != VER)) return;
@@ -521,7 +534,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   // tile, so the per-q offset folds into the shared-memory address immediate
   // (row-like: k0 is a multiple of TP = 8, so slot (k0 + q) ^ swizzle = slot(k0) ^ q)
   auto tix = [&](int k0, int q) { return ROWLIKE ? (rix(lane, k0) ^ q) : pix(lane, k0) + (q << 5); };
-  const bool use_tma = !ROWLIKE && M.tma;
+  const bool use_tma = RT || (!ROWLIKE && M.tma);  // (RT: the host builds its maps)
   unsigned long long* mbar =
       reinterpret_cast<unsigned long long*>(base + 32 * RL * (8 + 2 * sizeof(ST)));
 
@@ -682,7 +695,9 @@ __global__ void __launch_bounds__(WARPS * 32)
         mbar_expect(bar, TP * 32 * (2 * sizeof(ST) + 8));
         tma2d((unsigned)__cvta_generic_to_shared(rp + slot), &M.p, (int)c0, k0, bar);
         tma2d((unsigned)__cvta_generic_to_shared(ra + slot), &M.a, (int)c0, k0, bar);
-        if (M.c3)
+        if (RT)  // (8 positions x 32 rows) of the natural drift, rows = the warp's chains
+          tma2d((unsigned)__cvta_generic_to_shared(rz + slot), &M.c, k0, (int)c0, bar);
+        else if (M.c3)
           tma3d((unsigned)__cvta_generic_to_shared(rz + slot), &M.c, cx0, k0, co0, bar);
         else
           tma2d((unsigned)__cvta_generic_to_shared(rz + slot), &M.c, (int)c0, k0, bar);
@@ -796,11 +811,30 @@ __global__ void __launch_bounds__(WARPS * 32)
     // the ring arrays apart, so an interleaved form serialises load -> store
     ST pv[TP];
     double cv[TP];
+    if (RT) {
+      // the drift box sits in the tile's z slots as [row = lane][8 positions],
+      // 64-B swizzled (16-B chunk j of a 64-B row at j ^ address bits 7-8):
+      // each lane reads its own row as four 16-B vectors (conflict free: the
+      // 8 lanes of a phase cover distinct bank quads), then, after every lane
+      // has read, the z values go to the [pos][lane] slots
+      const unsigned rb = rz_s + (unsigned)pix(0, T * TP) * 8u + (unsigned)lane * 64u;
 #pragma unroll
-    for (int q = 0; q < TP; ++q) {
-      const int ix = tix(T * TP, q);
-      pv[q] = rp[ix];
-      cv[q] = rz[ix];
+      for (int j = 0; j < TP / 2; ++j) {
+        const unsigned a = rb + (unsigned)j * 16u;
+        const unsigned ph = a ^ (((a >> 7) & 3u) << 4);
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n"
+                     : "=d"(cv[2 * j]), "=d"(cv[2 * j + 1]) : "r"(ph) : "memory");
+      }
+#pragma unroll
+      for (int q = 0; q < TP; ++q) pv[q] = rp[tix(T * TP, q)];
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int q = 0; q < TP; ++q) {
+        const int ix = tix(T * TP, q);
+        pv[q] = rp[ix];
+        cv[q] = rz[ix];
+      }
     }
 #pragma unroll
     for (int q = 0; q < TP; ++q) rz[tix(T * TP, q)] = (double)pv[q] + cv[q];
@@ -858,7 +892,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
         const double pn = (zj - zs) + qs;
         if (ROLE == SHADOW) {
-          if (!ROWLIKE) A.y[node(base32, pos)] = pn;
+          if (!ROWLIKE && !RT) A.y[node(base32, pos)] = pn;
           else ysv[q] = pn;
         } else {
           const ST pold = rp[ix];
@@ -869,7 +903,9 @@ __global__ void __launch_bounds__(WARPS * 32)
           const double d = (double)dS;
           nq = nrm_d(d, nq);
           A.po[pi0 + q * C32] = p32;
-          if (!ROWLIKE) {
+          if (RT) {
+            dsv[q] = dS;
+          } else if (!ROWLIKE) {
             const int nd = nd0 + q * ns32;  // strided: node(base32, k0 + q)
             if (ROLE == FIRST) {
               A.G[nd] = dS;
@@ -897,6 +933,39 @@ __global__ void __launch_bounds__(WARPS * 32)
         if (FULL || ((emask >> q) & 1u)) {
           if (ROLE == SHADOW) rz[ixb ^ q] = ysv[q];
           else ra[ixb ^ q] = dsv[q];
+        }
+      }
+    }
+    if (RT) {  // the tile's node-order outputs: this lane's row, positions k0..k0+7
+      if (FULL) {  // 16-B vectors (pcb_create keeps row starts 4-element aligned for RT)
+        if (ROLE == SHADOW) {
+          double* yp = A.y + nd0;
+#pragma unroll
+          for (int j = 0; j < TP / 2; ++j)
+            asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(yp + 2 * j),
+                         "d"(ysv[2 * j]), "d"(ysv[2 * j + 1]) : "memory");
+        } else {
+          ST* gp = A.G + nd0;
+          if (sizeof(ST) == 4) {
+#pragma unroll
+            for (int j = 0; j < TP / 4; ++j)
+              asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(gp + 4 * j),
+                           "f"((float)dsv[4 * j]), "f"((float)dsv[4 * j + 1]),
+                           "f"((float)dsv[4 * j + 2]), "f"((float)dsv[4 * j + 3]) : "memory");
+          } else {
+#pragma unroll
+            for (int j = 0; j < TP / 2; ++j)
+              asm volatile("st.global.v2.f64 [%0], {%1, %2};\n" ::"l"(gp + 2 * j),
+                           "d"((double)dsv[2 * j]), "d"((double)dsv[2 * j + 1]) : "memory");
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < TP; ++q) {
+          if ((emask >> q) & 1u) {
+            if (ROLE == SHADOW) A.y[nd0 + q] = ysv[q];
+            else A.G[nd0 + q] = dsv[q];
+          }
         }
       }
     }

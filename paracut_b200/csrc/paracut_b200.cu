@@ -1626,7 +1626,7 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
-template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float>
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false>
 int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fast::Maps& M) {
   pcb::fast::ArgsT<ST> a = a_in;
   pcb::fast::args_inplace(a);
@@ -1638,7 +1638,7 @@ int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fas
   static unsigned set_mask = 0;
   const unsigned bit = 1u << (h->device & 31);
   if (!(set_mask & bit)) {
-    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST>,
+    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     set_mask |= bit;
   }
@@ -1655,18 +1655,29 @@ int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fas
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST>, a, M));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT>, a, M));
   } else {
-    pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST><<<g, per, bytes, h->stream>>>(a, M);
+    pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT><<<g, per, bytes, h->stream>>>(a, M);
   }
   LAUNCH_CHECK(h);
   return 0;
 }
 
+// a row family with a row map (Maps::row) in the first or shadow role runs
+// the row-TMA sweep; other row-like families (zig-zags, later roles) the
+// per-lane cp.async one
+template <int ROLE, class ST>
+int launch_rowlike(pcb_solver* h, const pcb::fast::ArgsT<ST>& a, const pcb::fast::Maps& M) {
+  if constexpr (ROLE == pcb::fast::FIRST || ROLE == pcb::fast::SHADOW) {
+    if (M.row && M.tma) return launch_sweep<ROLE, false, false, ST, true>(h, a, M);
+  }
+  return launch_sweep<ROLE, true, false, ST>(h, a, M);
+}
+
 template <int ROLE, class ST>
 int launch_role(pcb_solver* h, const pcb::fast::ArgsT<ST>& a, int j) {
   pcb::fast::Maps* M = FastState<ST>::maps(h);
-  return fam_rowlike(a.F.kind) ? launch_sweep<ROLE, true, false, ST>(h, a, M[j])
+  return fam_rowlike(a.F.kind) ? launch_rowlike<ROLE, ST>(h, a, M[j])
                                : launch_sweep<ROLE, false, false, ST>(h, a, M[j]);
 }
 
@@ -1699,7 +1710,7 @@ int launch_role_v(pcb_solver* h, const pcb::fast::ArgsT<ST>& a, int j) {
     return launch_role<ROLE, ST>(h, a, j);
   } else {
   const bool rl = fam_rowlike(a.F.kind);
-  if (int e = rl ? launch_sweep<ROLE, true>(h, a, h->maps[j]) : launch_sweep<ROLE, false>(h, a, h->maps[j]))
+  if (int e = rl ? launch_rowlike<ROLE, float>(h, a, h->maps[j]) : launch_sweep<ROLE, false>(h, a, h->maps[j]))
     return e;
   if (!a.vmode) return 0;
   if (verify_ring())
@@ -1781,8 +1792,37 @@ void build_maps_for(pcb_solver* h, ST* pbuf, double* cbuf, pcb::fast::Maps* maps
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return;
   using pcb::fast::TP;
+  const char* renv = getenv("PCB_ROW_TMA");  // A/B knob: 0 keeps rows on cp.async
+  const bool row_tma = !(renv && renv[0] == '0');
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
+    if ((F.kind == K_ROW2 || F.kind == K_X3) && row_tma && F.zz == 0 && F.ns == 1 &&
+        F.cdiv == 1 && F.clo == 0 && F.chi == F.m && F.C % 32 == 0 && F.m % 4 == 0) {
+      // row family: chain c is the node row [c*m, (c+1)*m) (the vector stores
+      // of the RT retire need 16-B aligned row starts: m % 4 == 0)
+      pcb::fast::Maps M{};
+      const cuuint32_t box2[2] = {32, (cuuint32_t)TP}, es2[2] = {1, 1};
+      const cuuint64_t dp[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
+      const cuuint64_t da[2] = {(cuuint64_t)F.C, (cuuint64_t)(F.m - 1)};
+      const cuuint64_t sp[1] = {(cuuint64_t)F.C * sizeof(ST)};
+      CUresult r1 = fn(&M.p, ET, 2, (void*)(pbuf + (int64_t)j * h->n), dp, sp, box2, es2,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r2 = fn(&M.a, ET, 2, (void*)FastState<ST>::wf(h, j), da, sp, box2, es2,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      const cuuint64_t dc[2] = {(cuuint64_t)F.m, (cuuint64_t)F.C};
+      const cuuint64_t sc[1] = {(cuuint64_t)F.m * 8};
+      const cuuint32_t boxc[2] = {(cuuint32_t)TP, 32};
+      CUresult r3 = fn(&M.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)cbuf, dc, sc, boxc, es2,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS) continue;
+      M.tma = 1;
+      M.row = 1;
+      maps[j] = M;
+      continue;
+    }
     if (fam_rowlike(F.kind) || F.zz != 0 || F.C % 32 != 0 || F.m < 2) continue;
     bool c3;
     if (F.cdiv == 1 && F.chi == 1 && F.clo == 0)
