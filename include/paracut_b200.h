@@ -283,6 +283,14 @@ int pcb_level_set(pcb_solver *h, const double *x, double *u, double *energy);
  * handle precision. */
 int pcb_project_K(pcb_solver *h, const double *v, double *out);
 
+/* Plain iterations of the f32 / f64s paths replay as CUDA graphs of 8
+ * iterations once the handle has run `iters` of them eagerly (default 64:
+ * capture and instantiation cost about as much as the replays save over 80
+ * iterations, so short solves stay eager).  0 = capture on the first block
+ * (steady-state measurements).  No reference counterpart: the reference loop
+ * (solvers.py:289-298) has no launch overhead to hide. */
+int pcb_set_graph_after(pcb_solver *h, int64_t iters);
+
 /* Kernel timing for the roofline: while enabled, every chain-family prox
  * launch is bracketed by CUDA events on the handle stream; pcb_profile_read
  * synchronises, returns summed milliseconds and launch counts per family

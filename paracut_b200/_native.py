@@ -75,6 +75,7 @@ def _declare(L):
     L.pcb_project_K.argtypes = [P, P, P]
     L.pcb_project_L.argtypes = [P, P, P, INT, I64, P, P, INT]
     L.pcb_set_profiling.argtypes = [P, INT]
+    L.pcb_set_graph_after.argtypes = [P, I64]
     L.pcb_profile_read.argtypes = [P, P, P]
     L.pcb_verify_stats.argtypes = [P, P, P, P, P, P]
     L.pcb_apply_g_exchange.argtypes = [P, ctypes.c_size_t, ctypes.c_size_t, INT, INT, INT]
@@ -106,7 +107,8 @@ EXPORTS = ("pcb_last_error", "pcb_version", "pcb_device_count", "pcb_prox_chains
            "pcb_reset_launch_count", "pcb_jaccard_packed", "pcb_set_owned", "pcb_log_start",
            "pcb_log_stop", "pcb_log_norms", "pcb_log_labels", "pcb_log_label_get",
            "pcb_log_jaccard", "pcb_verify_stats", "pcb_create_synthetic", "pcb_get_instance",
-           "pcb_apply_g_exchange", "pcb_create_synthetic_box", "pcb_clone", "pcb_copy_state")
+           "pcb_apply_g_exchange", "pcb_create_synthetic_box", "pcb_clone", "pcb_copy_state",
+           "pcb_set_graph_after")
 
 
 def lib():
@@ -296,6 +298,11 @@ class GridSolver:
     # -- state
     def set_stream(self, stream_ptr):
         check(lib().pcb_set_stream(self.handle, int(stream_ptr)))
+
+    def set_graph_after(self, iters):
+        """Plain iterations replay as CUDA graphs once the handle has run
+        ``iters`` of them eagerly (default 64; 0: from the first block)."""
+        check(lib().pcb_set_graph_after(self.handle, int(iters)))
 
     def synchronize(self):
         check(lib().pcb_synchronize(self.handle))

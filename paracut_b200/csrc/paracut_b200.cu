@@ -1218,6 +1218,11 @@ struct pcb_solver {
   cudaStream_t gstream = nullptr;
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   int64_t glaunches[2] = {0, 0};  // kernel launches in each graph
+  // graphs are captured once the handle has run this many plain iterations
+  // eagerly (capture + instantiate cost about 80 iterations' worth of the
+  // replay's saving: short solves never pay it); pcb_set_graph_after
+  int64_t graph_after = 64;
+  int64_t plain_done = 0;  // plain (flags == 0) iterations run on this handle
   DBuf<double> gnorms;
   int64_t merge_off[MAXR]{};
   // merges of a step run on a side stream, overlapping the sweeps (they
@@ -2908,6 +2913,16 @@ bool graphs_enabled() {
   return v == 1;
 }
 
+// PCB_GRAPH_AFTER=N overrides every handle's capture threshold (experiments)
+int64_t graph_after_env() {
+  static int64_t v = -2;
+  if (v == -2) {
+    const char* e = getenv("PCB_GRAPH_AFTER");
+    v = (e && e[0]) ? (int64_t)atoll(e) : -1;
+  }
+  return v;
+}
+
 // GRAPH_STEPS iterations replayed from a CUDA graph captured on first use (the
 // step's launches -- sweeps, merges on the side stream, reductions, mode
 // words -- become one graph launch); norms land in h->gnorms.
@@ -2971,15 +2986,27 @@ int pcb_aar_step(pcb_solver* h, int64_t iters, int flags, double* step_norms) {
   h->sweeps_ev_ok = false;  // other work may have touched the state since the last step
   const bool use_graph = flags == 0 && !h->profiling && graphs_enabled() && h->precision != PCB_F64;
   int64_t k = 0;
-  if (use_graph)
+  if (use_graph) {
+    // eager until the handle has run graph_after plain iterations (a graph
+    // that exists already is replayed at once)
+    const int64_t after = graph_after_env() >= 0 ? graph_after_env() : h->graph_after;
+    if (!h->gexec[h->par] && h->plain_done < after) {
+      // (whole blocks of the eager part keep the double-buffered parity)
+      const int64_t need = after - h->plain_done;
+      const int64_t eager = std::min(iters, (need + GRAPH_STEPS - 1) / GRAPH_STEPS * GRAPH_STEPS);
+      for (; k < eager; ++k)
+        if (int rc = one_step(h, nout + k, flags)) return rc;
+    }
     for (; k + GRAPH_STEPS <= iters; k += GRAPH_STEPS) {
       if (int rc = graph_steps(h)) return rc;
       h->sweeps_ev_ok = false;  // (recorded inside the capture, not at this replay)
       CUDA_TRY(cudaMemcpyAsync(nout + k, h->gnorms.p, GRAPH_STEPS * sizeof(double),
                                cudaMemcpyDeviceToDevice, h->stream));
     }
+  }
   for (; k < iters; ++k)
     if (int rc = one_step(h, nout + k, flags)) return rc;
+  if (flags == 0) h->plain_done += iters;
   if (to_log) h->nlog += iters;
   h->have_shadow = false;
   h->y_valid = false;
@@ -3575,6 +3602,13 @@ int pcb_verify_stats(pcb_solver* h, int* modes, int64_t* sweeps, int64_t* repair
     if (scans) scans[j] = st[4 * j + 2];
     if (changed) changed[j] = st[4 * j + 3];
   }
+  return 0;
+}
+
+int pcb_set_graph_after(pcb_solver* h, int64_t iters) {
+  if (!h) return fail(PCB_E_ARG, "null handle");
+  if (iters < 0) return fail(PCB_E_ARG, "iters must be >= 0");
+  h->graph_after = iters;
   return 0;
 }
 

@@ -239,3 +239,31 @@ def test_clone_and_copy_state_device_handover():
         h.init_cold()
         h.run(5, norms=False)
     assert np.array_equal(V.get_z(), W.get_z())
+
+
+@pytest.mark.parametrize("precision", ["f32", "f64s"])
+def test_graph_replay_equals_eager_iterations(precision):
+    # plain iterations replay as CUDA graphs once a handle has run 64 of them
+    # (pcb_set_graph_after); replays and eager launches are the same kernels
+    from paracut_b200 import _native
+    g = make_instance(CONFIGS["cfg4"], seed=3, dims=(40, 36, 44))
+    out = []
+    for after in (0, 1 << 30):  # graphs from the first block / never
+        S = _native.GridSolver(g, precision=precision)
+        S.set_graph_after(after)
+        S.init_cold()
+        norms = np.concatenate([S.run(24), S.run(5), S.run(16)])
+        out.append((S.get_z(), norms))
+        S.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    # default threshold: the first 64 iterations run eagerly, later blocks replay
+    S = _native.GridSolver(g, precision=precision)
+    S.init_cold()
+    norms = np.concatenate([S.run(24), S.run(5), S.run(16), S.run(40)])
+    S2 = _native.GridSolver(g, precision=precision)
+    S2.set_graph_after(1 << 30)
+    S2.init_cold()
+    norms2 = S2.run(85)
+    assert np.array_equal(S.get_z(), S2.get_z())
+    assert np.array_equal(norms, norms2)
