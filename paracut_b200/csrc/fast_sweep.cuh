@@ -497,12 +497,16 @@ __device__ __noinline__ double repair_lane(const Args& A, int c32, int base32, i
 // RT: a row family fed by TMA (Maps::row); it runs the strided families'
 // [pos][lane] ring (ROWLIKE = false), with the drift box transposed in to_z
 // and its node-order outputs stored as per-lane vectors along the row.
-template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false>
+// XG: the LAST role also stores its per-node g = sum_j d_j in G (sharded
+// runs, PCB_STEP_EXPORT_G); compiled in, so the plain step carries no test
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false,
+          bool XG = false>
 __global__ void __launch_bounds__(WARPS * 32)
     k_sweep(const __grid_constant__ ArgsT<ST> A, const __grid_constant__ Maps M) {
   static_assert(!VER || sizeof(ST) == 4, "verified sweeps run in the fp32-state mode");
   static_assert(!RT || (!ROWLIKE && !VER && (ROLE == FIRST || ROLE == SHADOW)),
                 "row-TMA sweeps: first family or shadow only");
+  static_assert(!XG || ROLE == LAST, "only the LAST role exports g");
   constexpr bool S64 = sizeof(ST) == 8;  // fp64 state (f64s): fp64 scan, fp64 ring slots
   extern __shared__ __align__(1024) unsigned char smem_raw[];  // TMA boxes land 512-B aligned
   // device-side choice between the two sweeps of a family (both are launched;
@@ -853,6 +857,31 @@ __global__ void __launch_bounds__(WARPS * 32)
     // G / X / c in node order
     const int pi0 = k0 * C32 + c32;
     const int nd0 = node(base32, k0);
+    // per-tile output bases kept in registers (opaque to the compiler, which
+    // otherwise re-reads the argument pointers from the constant bank and
+    // rebuilds a 64-bit address from the element index at every position):
+    // a position's store address is then one IMAD.WIDE off the base
+    ST* po_t = A.po + pi0;
+    ST* G_t = A.G + nd0;
+    ST* Xo_t = A.Xo + nd0;
+    double* co_t = A.co + nd0;
+#ifndef PCB_NO_RETIRE_BASES
+    if (ROLE != SHADOW) {
+      asm volatile("" : "+l"(po_t));
+      if (!ROWLIKE && !RT) {
+        if (ROLE != LAST || XG) asm volatile("" : "+l"(G_t));
+        if (ROLE == LAST) {
+          asm volatile("" : "+l"(Xo_t));
+          asm volatile("" : "+l"(co_t));
+        }
+      }
+      // (still global memory: keeps the stores STG rather than generic ST)
+      __builtin_assume(__isGlobal(po_t));
+      __builtin_assume(__isGlobal(G_t));
+      __builtin_assume(__isGlobal(Xo_t));
+      __builtin_assume(__isGlobal(co_t));
+    }
+#endif
     // strided families: the tile's ring rows are 32 slots apart from a per-tile
     // base, so every per-position ring access is base + immediate
     const int ixb = ROWLIKE ? rix(lane, k0) : pix(lane, k0);
@@ -902,23 +931,23 @@ __global__ void __launch_bounds__(WARPS * 32)
           const ST dS = p32 - pold;
           const double d = (double)dS;
           nq = nrm_d(d, nq);
-          A.po[pi0 + q * C32] = p32;
+          po_t[q * C32] = p32;
           if (RT) {
             dsv[q] = dS;
           } else if (!ROWLIKE) {
-            const int nd = nd0 + q * ns32;  // strided: node(base32, k0 + q)
+            const int nd = q * ns32;  // strided: node(base32, k0 + q) - nd0
             if (ROLE == FIRST) {
-              A.G[nd] = dS;
+              G_t[nd] = dS;
             } else if (ROLE == MID) {
-              A.G[nd] = gpre[q] + dS;
+              G_t[nd] = gpre[q] + dS;
             } else {
               const ST g32 = gpre[q] + dS;
               const double g = (double)g32;
               const double xn = (double)xpre[q] - g;
-              A.Xo[nd] = (ST)xn;
+              Xo_t[nd] = (ST)xn;
               const double dcv = (xn - g) * A.inv_r;
-              A.co[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
-              if (A.export_g) A.G[nd] = g32;
+              co_t[nd] = (zj - (double)pold) + dcv;  // c_old = z - p_old
+              if (XG) G_t[nd] = g32;
               nq = nrm_last(dcv, g, A.rd, nq);
             }
           } else {
@@ -1010,7 +1039,7 @@ __global__ void __launch_bounds__(WARPS * 32)
             A.Xo[nd] = (ST)xn;
             const double dcv = (xn - g) * A.inv_r;
             A.co[nd] = (rz[ix] - (double)rp[ix]) + dcv;  // c_old = z - p_old
-            if (A.export_g) A.G[nd] = g32;
+            if (XG) A.G[nd] = g32;
             double& nq = (ib & 1) ? nb : na;
             nq = nrm_last(dcv, g, A.rd, nq);
           }

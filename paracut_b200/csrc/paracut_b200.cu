@@ -1631,8 +1631,12 @@ int apply_fast(pcb_solver* h, double* norm_slot) {
   return 0;
 }
 
-template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false>
+template <int ROLE, bool ROWLIKE, bool VER = false, class ST = float, bool RT = false,
+          bool XG = false>
 int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fast::Maps& M) {
+  if constexpr (ROLE == pcb::fast::LAST && !XG && !VER) {  // the exporting variant of LAST
+    if (a_in.export_g) return launch_sweep<ROLE, ROWLIKE, VER, ST, RT, true>(h, a_in, M);
+  }
   pcb::fast::ArgsT<ST> a = a_in;
   pcb::fast::args_inplace(a);
 #ifndef PCB_RING_PAD
@@ -1643,7 +1647,7 @@ int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fas
   static unsigned set_mask = 0;
   const unsigned bit = 1u << (h->device & 31);
   if (!(set_mask & bit)) {
-    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT>,
+    CUDA_TRY(cudaFuncSetAttribute(pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT, XG>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     set_mask |= bit;
   }
@@ -1660,9 +1664,9 @@ int launch_sweep(pcb_solver* h, const pcb::fast::ArgsT<ST>& a_in, const pcb::fas
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT>, a, M));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT, XG>, a, M));
   } else {
-    pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT><<<g, per, bytes, h->stream>>>(a, M);
+    pcb::fast::k_sweep<ROLE, ROWLIKE, VER, ST, RT, XG><<<g, per, bytes, h->stream>>>(a, M);
   }
   LAUNCH_CHECK(h);
   return 0;
