@@ -552,7 +552,15 @@ __global__ void __launch_bounds__(WARPS * 32)
   // index and interleaved index pos * C + c fits (half the address IMADs)
   const int C32 = (int)F.C, c32 = (int)c;
   const int ns32 = (int)F.ns, zz32 = (int)F.zz, ph32 = F.phase;
+#ifdef PCB_DIV64
   const int base32 = valid ? (int)fam_base(F, c) : 0;
+#else
+  // (n < 2^31: chain index, cdiv and the base fit in 32 bits; the 64-bit
+  // division of fam_base is ~100 instructions)
+  const unsigned cdv = (unsigned)F.cdiv;
+  const unsigned cq = (unsigned)c32 / cdv, cr = (unsigned)c32 - cq * cdv;
+  const int base32 = valid ? (int)(cq * (unsigned)F.chi + cr * (unsigned)F.clo) : 0;
+#endif
   // zig-zag families are row-like, so strided families have no zig-zag term
   auto node = [&](int b, int pos) {
     return ROWLIKE ? b + pos * ns32 + zz32 * ((pos + ph32) & 1) : b + pos * ns32;
@@ -646,7 +654,12 @@ __global__ void __launch_bounds__(WARPS * 32)
   int pre_tile = -1;
 
   int t_lo = t_first, t_ld = t_first, t_rdy = t_first;
+#ifdef PCB_DIV64
   const int cx0 = (int)(c0 % F.cdiv), co0 = (int)(c0 / F.cdiv);  // TMA box origin of c
+#else
+  const int co0 = (int)((unsigned)c0 / (unsigned)F.cdiv);  // TMA box origin of c
+  const int cx0 = (int)((unsigned)c0 - (unsigned)co0 * (unsigned)F.cdiv);
+#endif
   if (use_tma && warp_live) {
     if (lane == 0) {
       for (int u = 0; u < NT; ++u) mbar_init((unsigned)__cvta_generic_to_shared(&mbar[u]), 1);
@@ -678,15 +691,13 @@ __global__ void __launch_bounds__(WARPS * 32)
       const unsigned sh = (unsigned)(T & (NT - 1)) * 16u;
       sw = (sw & ~(0xffffull << sh)) | ((unsigned long long)A.sg[T * C32 + c32] << sh);
     }
-    if (ROLE == MID || ROLE == LAST) {
+    // (row-like families only: the strided families' retire inputs are one
+    // 128-byte line per position and array, and their register prefetch a
+    // round ahead hides DRAM by itself -- cfg4 z 0.1729 -> 0.1696 ms without)
+    if (ROWLIKE && (ROLE == MID || ROLE == LAST)) {
       // pull the tile's retire-only inputs (G, X: natural layout) towards L2
       // now, so the register prefetch a round before retirement hits L2
-      if (!ROWLIKE) {  // 32 chains = 32 consecutive nodes per position: lanes 0-7 G, 8-15 X
-        const int q = lane & 7, pos = k0 + q;
-        if (warp_live && pos < m && (lane < 8 || (ROLE == LAST && lane < 16)))
-          l2_prefetch((lane < 8 ? (const void*)(A.Gi + node(b0, pos))
-                                : (const void*)(A.X + node(b0, pos))));
-      } else if (valid && k0 < m) {  // each lane: its chain's 8 positions
+      if (valid && k0 < m) {  // each lane: its chain's 8 positions
         l2_prefetch(A.Gi + node(base32, k0));
         if (ROLE == LAST) l2_prefetch(A.X + node(base32, k0));
       }
@@ -695,7 +706,9 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (lane == 0) {
         const unsigned bar = (unsigned)__cvta_generic_to_shared(&mbar[(T - t_first) & (NT - 1)]);
         const int slot = (T & (NT - 1)) * TP * 32;
+#ifndef PCB_NO_PROXY_FENCE  // (experiment knob: the fence's cost)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // ring was read generically
+#endif
         mbar_expect(bar, TP * 32 * (2 * sizeof(ST) + 8));
         tma2d((unsigned)__cvta_generic_to_shared(rp + slot), &M.p, (int)c0, k0, bar);
         tma2d((unsigned)__cvta_generic_to_shared(ra + slot), &M.a, (int)c0, k0, bar);
@@ -787,6 +800,18 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     const int k0 = T * TP;
     if (!ROWLIKE) {
+      if (nvalid == 32 && k0 + TP <= m) {
+        // whole tile of a full warp (the usual case): no predicates, one
+        // per-tile base per array and one IMAD.WIDE + load per position
+        const ST* gi_t = A.Gi + (base32 + k0 * ns32);
+        const ST* x_t = A.X + (base32 + k0 * ns32);
+#pragma unroll
+        for (int q = 0; q < TP; ++q) {
+          gpre[q] = gi_t[q * ns32];
+          if (ROLE == LAST) xpre[q] = x_t[q * ns32];
+        }
+        return;
+      }
 #pragma unroll
       for (int q = 0; q < TP; ++q) {
         const int pos = k0 + q;
