@@ -1788,6 +1788,20 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+// A row family (chain c is the node row [c*m, (c+1)*m)) that gets the row map
+// of the TMA-fed sweep (k_sweep<..., RT>): full warps, and 16-B aligned row
+// starts for the retire's vector stores (m % 4 == 0).  PCB_TMA=0 /
+// PCB_ROW_TMA=0 keep it on per-lane cp.async.
+bool row_tma_family(const Fam& F) {
+  const char* env = getenv("PCB_TMA");
+  if (env && env[0] == '0') return false;
+  const char* renv = getenv("PCB_ROW_TMA");
+  if (renv && renv[0] == '0') return false;
+  if (!encode_tiled()) return false;
+  return (F.kind == K_ROW2 || F.kind == K_X3) && F.zz == 0 && F.ns == 1 && F.cdiv == 1 &&
+         F.clo == 0 && F.chi == F.m && F.C % 32 == 0 && F.m % 4 == 0;
+}
+
 // TMA maps for the strided families whose warps cover 32 consecutive nodes
 // (cols; 3D y with D2 % 32 == 0; 3D z).  Others keep the per-lane cp.async.
 // PCB_TMA=0 disables them.
@@ -1801,14 +1815,9 @@ void build_maps_for(pcb_solver* h, ST* pbuf, double* cbuf, pcb::fast::Maps* maps
   EncodeTiledFn fn = encode_tiled();
   if (!fn) return;
   using pcb::fast::TP;
-  const char* renv = getenv("PCB_ROW_TMA");  // A/B knob: 0 keeps rows on cp.async
-  const bool row_tma = !(renv && renv[0] == '0');
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
-    if ((F.kind == K_ROW2 || F.kind == K_X3) && row_tma && F.zz == 0 && F.ns == 1 &&
-        F.cdiv == 1 && F.clo == 0 && F.chi == F.m && F.C % 32 == 0 && F.m % 4 == 0) {
-      // row family: chain c is the node row [c*m, (c+1)*m) (the vector stores
-      // of the RT retire need 16-B aligned row starts: m % 4 == 0)
+    if (row_tma_family(F)) {
       pcb::fast::Maps M{};
       const cuuint32_t box2[2] = {32, (cuuint32_t)TP}, es2[2] = {1, 1};
       const cuuint64_t dp[2] = {(cuuint64_t)F.C, (cuuint64_t)F.m};
@@ -2163,11 +2172,13 @@ int setup_verify(pcb_solver* h) {
   bool any = false;
   for (int j = 0; j < h->r; ++j) {
     const Fam& F = h->fam[j];
-    // row-like families only: their scan stages c through per-lane cp.async
-    // rows, where the verified sweep's contiguous vector loads win; the
-    // strided families' TMA-fed scan is as fast as a verified sweep
+    // row families on per-lane cp.async only: there the verified sweep's
+    // contiguous vector loads win; the TMA-fed scans (strided families, and
+    // row families with a row map) are as fast as a verified sweep or faster
+    // (cfg5 x family: 0.96 ms verified, 0.92 ms row-TMA scan), and a step
+    // without verified families keeps its programmatic launches
     if (F.C == 0 || F.m < 2 || h->nbk[j] > 1 || !fam_rowlike(F.kind) || F.kind == K_ZZ0 ||
-        F.kind == K_ZZ1 || F.m >= (1 << 16))
+        F.kind == K_ZZ1 || F.m >= (1 << 16) || row_tma_family(F))
       continue;
     const int64_t cnt = (int64_t)((F.m + pcb::fast::TP - 1) / pcb::fast::TP) * F.C;
     if (int e = h->sg[j].alloc(cnt)) return e;
