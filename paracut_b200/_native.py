@@ -434,9 +434,15 @@ class GridSolver:
     def keep_best(self, t):
         check(lib().pcb_keep_best(self.handle, int(t)))
 
-    def get_best(self, labels=True, x=True):
-        """(labels uint8, x fp64) of the kept best iterate; either may be skipped (None)."""
-        lab = _host_empty((self.n,), np.uint8) if labels else None
+    def get_best(self, labels=True, x=True, labels_out=None):
+        """(labels uint8, x fp64) of the kept best iterate; either may be skipped (None).
+        ``labels_out``: a uint8 host array of n entries to fill (e.g. one whose
+        pages were touched while the device was busy)."""
+        lab = None
+        if labels:
+            ok = (isinstance(labels_out, np.ndarray) and labels_out.dtype == np.uint8
+                  and labels_out.shape == (self.n,) and labels_out.flags.c_contiguous)
+            lab = labels_out if ok else _host_empty((self.n,), np.uint8)
         xv = _host_empty((self.n,)) if x else None
         check(lib().pcb_get_best(self.handle, ptr(lab) if labels else None,
                                  ptr(xv) if x else None))

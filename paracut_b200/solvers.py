@@ -234,7 +234,17 @@ class _Driver:
         self.stall = 0  # > 0: leave the loop once the best gap stalls for this many checks
         self._best_hist = []
         self.log = False  # solve log on the device (start_log)
+        self._lab_buf = None  # the result's labeling, pages touched ahead (prefault_labels)
         self.t0 = time.perf_counter()
+
+    def prefault_labels(self):
+        """Allocate the result's label array and touch its pages now.  Called
+        right after iterations were queued on the device, so the first-touch
+        page faults (the larger part of the final read-back of a fresh array)
+        run on the host while the device works."""
+        if self._lab_buf is None:
+            self._lab_buf = np.empty(self.g.n, dtype=np.uint8)
+            self._lab_buf.fill(0)
 
     def start_log(self):
         """Keep step norms and check labelings on the device (pcb_log_*): a check
@@ -347,7 +357,8 @@ class _Driver:
         wall = time.perf_counter() - self.t0
         src = self.best_solver or self.solver
         lazy_x = self.owned  # no later solve reuses the handle: x on first access
-        lab, x = src.get_best(labels=True, x=not lazy_x)
+        lab, x = src.get_best(labels=True, x=not lazy_x, labels_out=self._lab_buf)
+        self._lab_buf = None
         certified = self.best_gap <= self.cfg.gap_tol + GAP_SLACK
         if self.cfg.reference is None and self.log:
             self.flush_norms()
@@ -448,7 +459,8 @@ def _loop(drv, S, k, checked=None):
         else:
             nxt = drv.next_due(k)
             if drv.log:
-                S.run(nxt - k, norms=False)
+                S.run(nxt - k, norms=False)  # queued; the host is free until the next check
+                drv.prefault_labels()
             else:
                 drv.record("aar_step_norm", S.run(nxt - k))
             k = nxt
