@@ -567,7 +567,6 @@ __global__ void __launch_bounds__(WARPS * 32)
   };
   // mode B (row-like families): lane works on chains 8*(lane/8) + ib, ib < 8;
   // their node bases are fixed for the whole launch
-  const int b0 = __shfl_sync(0xffffffffu, base32, 0);  // lane 0's chain base
   int bB[8];
   if (ROWLIKE) {
 #pragma unroll
