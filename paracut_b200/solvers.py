@@ -323,9 +323,16 @@ class _Driver:
         self._best_hist.append(self.best_gap)
         return self.stopped
 
+    POLISH_NEAR = 10.0  # a best gap within this factor of the tolerance hands over at once
+
     def stalled(self):
-        """The best gap has not halved over the last `stall` checks."""
+        """The best gap has not halved over the last `stall` checks -- or it is
+        already within POLISH_NEAR of the tolerance, where only the fp32
+        state's noise floor can separate it from a certificate (cfg4: 1.3e-6
+        against 1e-6), so waiting for the stall to show buys nothing."""
         h, w = self._best_hist, self.stall
+        if w > 0 and h and h[-1] <= self.POLISH_NEAR * (self.cfg.gap_tol + GAP_SLACK):
+            return True
         if w > 0 and self.cfg.polish_gap > 0 and not h[-1] <= self.cfg.polish_gap:
             return False
         return w > 0 and len(h) > w and not h[-1] <= 0.5 * h[-1 - w]
