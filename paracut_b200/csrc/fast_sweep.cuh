@@ -161,6 +161,17 @@ __device__ __forceinline__ void tma3d(unsigned dst, const CUtensorMap* map, int 
       : "memory");
 }
 
+// p' of a whole tile as one bulk tensor store from the ring's p slots (the
+// row-TMA FIRST sweep)
+__device__ __forceinline__ void tma2d_store(const CUtensorMap* map, int x, int y, unsigned src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n"
+               "cp.async.bulk.commit_group;\n" ::"l"(map), "r"(x), "r"(y), "r"(src)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+
 // Predicated copies (no zero fill): slots of positions past the chain end or
 // of lanes without a chain are never read, so skipping them is enough and
 // avoids the src-size arithmetic of the zero-filling form.
@@ -508,6 +519,15 @@ __global__ void __launch_bounds__(WARPS * 32)
                 "row-TMA sweeps: first family or shadow only");
   static_assert(!XG || ROLE == LAST, "only the LAST role exports g");
   constexpr bool S64 = sizeof(ST) == 8;  // fp64 state (f64s): fp64 scan, fp64 ring slots
+  // TMA store of p' (UTMASTG): pays in the row-TMA FIRST sweep, whose retire has
+  // few other stores (cfg4 x 0.158 -> 0.154 ms, cfg5 0.921 -> 0.889); the MID /
+  // LAST sweeps lose 4-6 % to the wait before the slot's reload
+  // (profiles/r2/ab_tma_store.txt; PCB_TMA_STORE_ALL: every TMA-fed role)
+#ifdef PCB_TMA_STORE_ALL
+  constexpr bool TST = !ROWLIKE && !VER && ROLE != SHADOW;
+#else
+  constexpr bool TST = RT && ROLE == FIRST;
+#endif
   extern __shared__ __align__(1024) unsigned char smem_raw[];  // TMA boxes land 512-B aligned
   // device-side choice between the two sweeps of a family (both are launched;
   // the one the mode word does not select returns at once)
@@ -708,6 +728,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 #ifndef PCB_NO_PROXY_FENCE  // (experiment knob: the fence's cost)
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // ring was read generically
 #endif
+        if (TST) bulk_wait_read();  // this slot's p' store (issued by this lane) has read the ring
         mbar_expect(bar, TP * 32 * (2 * sizeof(ST) + 8));
         tma2d((unsigned)__cvta_generic_to_shared(rp + slot), &M.p, (int)c0, k0, bar);
         tma2d((unsigned)__cvta_generic_to_shared(ra + slot), &M.a, (int)c0, k0, bar);
@@ -919,6 +940,10 @@ __global__ void __launch_bounds__(WARPS * 32)
     // it would order every later ring load behind it
     ST dsv[TP];
     double ysv[TP];
+    // TST: the tile's p' goes through the ring's p slots and one bulk tensor
+    // store (in-place steps only: the output array is the map's)
+    ST psv[TP];
+    const bool tma_st = TST && use_tma && A.po == A.p;
 #pragma unroll
     for (int q = 0; q < TP; ++q) {
       const int pos = k0 + q;
@@ -955,7 +980,8 @@ __global__ void __launch_bounds__(WARPS * 32)
           const ST dS = p32 - pold;
           const double d = (double)dS;
           nq = nrm_d(d, nq);
-          po_t[q * C32] = p32;
+          if (TST && FULL && tma_st) psv[q] = p32;
+          else po_t[q * C32] = p32;
           if (RT) {
             dsv[q] = dS;
           } else if (!ROWLIKE) {
@@ -988,6 +1014,14 @@ __global__ void __launch_bounds__(WARPS * 32)
           else ra[ixb ^ q] = dsv[q];
         }
       }
+    }
+    if (TST && FULL && tma_st) {
+#pragma unroll
+      for (int q = 0; q < TP; ++q) rp[ixb + (q << 5)] = psv[q];
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> async reads
+      __syncwarp();
+      if (lane == 0)
+        tma2d_store(&M.p, (int)c0, k0, rp_s + (unsigned)pix(0, k0) * (unsigned)sizeof(ST));
     }
     if (RT) {  // the tile's node-order outputs: this lane's row, positions k0..k0+7
       if (FULL) {  // 16-B vectors (pcb_create keeps row starts 4-element aligned for RT)
@@ -1390,6 +1424,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int nch = __popc(__ballot_sync(0xffffffffu, hchanged && valid));
     if (lane == 0 && nch && A.vcount) atomicAdd(A.vcount, nch);
   }
+  // (the stores have read the ring before the block's shared memory goes away)
+  if (TST && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   if (ROLE != SHADOW) {  // step-norm partial: one slot per warp (no block barrier)
     const double v = warp_sum(nrm);
     if (lane == 0) A.parts[(blockIdx.x + (int64_t)blockIdx.y * gridDim.x) * WARPS + wib] = v;
