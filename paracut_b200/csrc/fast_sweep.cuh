@@ -521,8 +521,9 @@ __global__ void __launch_bounds__(WARPS * 32)
   constexpr bool S64 = sizeof(ST) == 8;  // fp64 state (f64s): fp64 scan, fp64 ring slots
   // TMA store of p' (UTMASTG): pays in the row-TMA FIRST sweep, whose retire has
   // few other stores (cfg4 x 0.158 -> 0.154 ms, cfg5 0.921 -> 0.889); the MID /
-  // LAST sweeps lose 4-6 % to the wait before the slot's reload
-  // (profiles/r2/ab_tma_store.txt; PCB_TMA_STORE_ALL: every TMA-fed role)
+  // LAST sweeps lose 4-6 % with it, with or without the wait before the
+  // slot's reload (profiles/r2/ab_tma_store.txt; PCB_TMA_STORE_ALL: every
+  // TMA-fed role)
 #ifdef PCB_TMA_STORE_ALL
   constexpr bool TST = !ROWLIKE && !VER && ROLE != SHADOW;
 #else
